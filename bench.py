@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""bench.py -- effective transpose GB/s (read+write) and % of HBM peak on 1..8 B200.
+
+Contract (task ③/④, BASELINE.json "metric"):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
+A "step" is one pass of the whole hot path over one batch of synthetic input: one
+C-ABI call (one kernel launch) transposing the workload's matrices.  Rank 0 prints ONE
+JSON line.  Under torchrun (N > 1) every rank transposes its own matrices (independent
+problems, no data-path collective: "scaling": "weak"); the time is the max over ranks.
+
+Default workload: 8192 x 8192 f32 (BASELINE.json configs[2], the headline target).
+Other workloads (--workload): 2048f64 (configs[1], L2-flushed), 3000x5000f64 (configs[2]),
+batched (configs[3], 256 x 1024^2 f32 sharded over ranks), dist65536 (configs[4]).
+
+--impl reference times the CPU oracle (oracle/, naive single-thread C loop) on the same
+workload -- the one other place bench.py executes oracle/ besides the cpu_baseline leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (seeded input generators only; no method arithmetic)
+
+METRIC = "transpose effective GB/s (read+write) and % of HBM peak at 1/2/4/8 B200"
+L2_BYTES = 126 * 1024 * 1024
+
+WORKLOADS = {
+    "8192f32": dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4,
+                    name="8192x8192 f32 transpose (BASELINE.json configs[2], headline target)"),
+    "2048f64": dict(batch=1, rows=2048, cols=2048, dtype="f64", es=8,
+                    name="2048x2048 f64 transpose (BASELINE.json configs[1], the paper's listing shape)"),
+    "3000x5000f64": dict(batch=1, rows=3000, cols=5000, dtype="f64", es=8,
+                         name="3000x5000 f64 non-tile-multiple transpose (BASELINE.json configs[2])"),
+    "batched": dict(batch=256, rows=1024, cols=1024, dtype="f32", es=4, shard=True,
+                    name="batched 256x(1024x1024) f32, batch sharded over ranks (BASELINE.json configs[3])"),
+}
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, read+write bytes)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload: str):
+    """dram bytes (read+write) per launch of the dominant kernel from the committed
+    `ncu --set full` summary, if one exists for this workload."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        v = d.get(workload)
+        return None if v is None else float(v["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.period = period_s
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def host_info():
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = os.cpu_count()
+    cpu = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu": cpu, "cpu_count": os.cpu_count(), "affinity": aff}
+
+
+# ------------------------------------------------------------------------- oracle arm
+def run_oracle(wl, budget_s: float, steps: int | None = None, warmup: int = 0,
+               band_rows: int | None = None, full_pass: bool = True):
+    """Time the oracle (naive single-thread C loop) on a bounded sample of the workload.
+
+    The sample is a sequence of row bands of the workload's matrices, each transposed by
+    the oracle into the FULL-size output buffer (same ld_out, so the access pattern is that
+    of the whole transpose).  With full_pass the bands cover every matrix of the sample once
+    (the output then is the complete oracle result, used for the parity check).
+    Returns dict(gbs, reps, sample, times, out, in)."""
+    import oracle
+    es, rows, cols, batch = wl["es"], wl["rows"], wl["cols"], wl["batch"]
+    sample_batch = min(batch, 4)
+    a = synth.random_bits((sample_batch, rows, cols), es, synth.BASE_SEED + 2)
+    out = np.empty((sample_batch, cols, rows), dtype=a.dtype)
+
+    def band(k, br):
+        nb = -(-rows // br)
+        m, b = divmod(k % (nb * sample_batch), nb)
+        r0 = b * br
+        r1 = min(rows, r0 + br)
+        t0 = time.perf_counter()
+        oracle.transpose_raw(a, out, 1, r1 - r0, cols, cols, rows, 0, 0, es,
+                             in_offset=m * rows * cols + r0 * cols,
+                             out_offset=m * cols * rows + r0)
+        return time.perf_counter() - t0, 2 * (r1 - r0) * cols * es
+
+    if band_rows is None:  # calibrate: seconds per row
+        dt, _ = band(0, 64)
+        per_row = max(dt / 64, 1e-7)
+        if steps:
+            band_rows = int(budget_s / (steps + warmup) / per_row)
+        else:
+            band_rows = rows
+        band_rows = max(8, min(rows, band_rows))
+    nbands = -(-rows // band_rows) * sample_batch
+    for k in range(warmup):
+        band(k, band_rows)
+    times, nbytes = [], 0
+    t_end = time.perf_counter() + budget_s
+    k = warmup
+    while True:
+        dt, b = band(k, band_rows)
+        times.append(dt)
+        nbytes += b
+        k += 1
+        if steps and len(times) >= steps:
+            break
+        if not steps and time.perf_counter() >= t_end and (not full_pass or k >= nbands):
+            break
+    gbs = nbytes / sum(times) / 1e9
+    desc = (f"{len(times)} row bands of {band_rows} x {cols} {wl['dtype']} "
+            f"(out of {sample_batch} of {batch} {rows}x{cols} matrices), each transposed into the "
+            f"full-size output (ld_out={rows}); GB/s = 2*bytes/sum(time)")
+    return dict(gbs=gbs, reps=len(times), sample=desc, times=times, out=out, inp=a,
+                complete=(k >= nbands and full_pass), band_rows=band_rows,
+                sample_batch=sample_batch)
+
+
+def reference_arm(args, wl, world, rank):
+    if rank != 0:
+        return 0
+    r = run_oracle(wl, budget_s=args.reference_seconds, steps=args.steps, warmup=args.warmup,
+                   full_pass=False)
+    hi = host_info()
+    ms = sum(r["times"]) / len(r["times"]) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(r["gbs"], 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": r["reps"], "warmup": args.warmup,
+        "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": wl["dtype"], "data": "synthetic (seeded random bit patterns)",
+        "config": {"workload": wl["name"], "rows": wl["rows"], "cols": wl["cols"],
+                   "batch": wl["batch"], "parallelism": "single host thread (CPU oracle)"},
+        "cpu_baseline": {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": 1,
+                         "kind": "oracle", "sample": r["sample"], "host": hi},
+        "e2e": {"value": round(r["gbs"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------- our arm
+def ours_arm(args, wl, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    import paper_2305_03448_b200 as desc
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    desc.load()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    es, rows, cols = wl["es"], wl["rows"], wl["cols"]
+    batch = wl["batch"]
+    if wl.get("shard"):
+        if batch % world:
+            raise SystemExit(f"batch {batch} not divisible by world {world}")
+        batch = batch // world
+    elem = {4: torch.int32, 8: torch.int64}[es]
+    tdt = {"f32": torch.float32, "f64": torch.float64, "i32": torch.int32}[wl["dtype"]]
+
+    # seeded synthetic input, generated on the host (so the oracle sees the same bits)
+    src = synth.random_bits((batch, rows, cols), es, synth.BASE_SEED + 2 + 1000 * rank)
+    src_t = torch.from_numpy(src.view(np.int32 if es == 4 else np.int64))
+    x = src_t.to(dev).view(tdt)
+    y = torch.empty((batch, cols, rows), dtype=tdt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    kernel = args.kernel
+    mat_bytes = rows * cols * es
+    step_bytes = 2 * batch * mat_bytes                     # algorithmic: read + write
+    flush = (batch * mat_bytes) < 2 * L2_BYTES
+    scratch = torch.empty(4 * L2_BYTES // 4, dtype=torch.int32, device=dev) if flush else None
+
+    def step():
+        if batch == 1:
+            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), 1, rows, cols, cols, rows, 0, 0,
+                                   wl["dtype"], kernel, sptr)
+        else:
+            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), batch, rows, cols, cols, rows,
+                                   rows * cols, rows * cols, wl["dtype"], kernel, sptr)
+        return desc.desc_last_launch_count()
+
+    selected = desc.desc_select_kernel(x.data_ptr(), y.data_ptr(), batch, rows, cols, cols, rows,
+                                       rows * cols if batch > 1 else 0,
+                                       rows * cols if batch > 1 else 0, wl["dtype"])
+    if kernel != "auto":
+        selected = kernel
+
+    for _ in range(args.warmup):
+        if flush:
+            scratch.fill_(0)
+        step()
+    torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    region0 = torch.cuda.Event(enable_timing=True)
+    region1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        region0.record(stream)
+        for k in range(args.steps):
+            if flush:
+                scratch.fill_(0)       # evict the 64 MiB working set from the 126 MB L2
+            starts[k].record(stream)
+            launches += step()
+            ends[k].record(stream)
+        region1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    per_launch = [s.elapsed_time(e) for s, e in zip(starts, ends)]   # ms, device time
+    region_ms = region0.elapsed_time(region1)
+    kern_ms_sum = sum(per_launch)
+    # timed quantity: the region (== sum of launches when there is no flush)
+    timed_ms = kern_ms_sum if flush else region_ms
+    t = torch.tensor([timed_ms, kern_ms_sum], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    timed_ms_max, kern_ms_max = t.tolist()
+
+    total_bytes = step_bytes * world * args.steps
+    value = total_bytes / (timed_ms_max / 1e3) / 1e9
+    avg_launch_ms = statistics.mean(per_launch)
+    achieved = step_bytes / (avg_launch_ms / 1e3) / 1e9
+    peak, peak_src = load_peak()
+
+    # ---- parity of the timed output (rank-local) ------------------------------------
+    parity = None
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_oracle:
+        r = run_oracle(wl, budget_s=args.oracle_seconds)
+        cpu_baseline = {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": 1,
+                        "kind": "oracle", "sample": r["sample"], "host": host_info()}
+        nb = r["sample_batch"]
+        got = y[:nb].view(elem).cpu().numpy().view(r["out"].dtype)
+        same_in = np.array_equal(r["inp"], src[:nb])
+        if not (same_in and r["complete"]):
+            parity = "not checked (oracle sample incomplete)"
+        else:
+            parity = ("bit-exact vs oracle" if got.tobytes() == r["out"].tobytes()
+                      else "MISMATCH vs oracle")
+
+    # ---- end to end through the public API with host buffers --------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, wl,
+                          kernel, world)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(timed_ms_max / args.steps, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": wl["dtype"], "data": "synthetic (seeded random bit patterns, host-generated)",
+            "config": {"workload": wl["name"], "rows": rows, "cols": cols,
+                       "batch_per_gpu": batch, "kernel": selected,
+                       "parallelism": f"{world} independent replica(s), no collective",
+                       "l2": ("flushed before every step (256 MiB write)" if flush else
+                              f"inputs larger than L2 ({batch * mat_bytes / 1e6:.0f} MB > 126 MB), no flush"),
+                       "timing": "CUDA events on the launch stream, max over ranks"},
+            "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": load_traffic(args.workload), "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": step_bytes,
+                         "kernel": f"transpose_{selected}_kernel",
+                         "launch_ms_median": round(statistics.median(per_launch), 5),
+                         "launch_ms_p10": round(float(np.percentile(per_launch, 10)), 5),
+                         "launch_ms_p90": round(float(np.percentile(per_launch, 90)), 5),
+                         "launch_ms_min": round(min(per_launch), 5)},
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "parity": parity,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, wl, kernel, world):
+    """Same metric end to end through desc_transpose_host: pinned host input -> device ->
+    transpose -> pinned host output, every step, inside the timed region."""
+    es = wl["es"]
+    h_in = src_t.pin_memory()
+    h_out = torch.empty((batch, cols, rows), dtype=src_t.dtype).pin_memory()
+    d_in = torch.empty((batch, rows, cols), dtype=tdt, device=dev)
+    d_out = torch.empty((batch, cols, rows), dtype=tdt, device=dev)
+    nbytes = batch * rows * cols * es
+    steps = max(3, min(args.steps, args.e2e_steps))
+
+    def one():
+        d_in.view(src_t.dtype).copy_(h_in, non_blocking=True)
+        if batch == 1:
+            desc.transpose(d_in[0], d_out[0], kernel=kernel)
+        else:
+            desc.transpose_batched(d_in, d_out, kernel=kernel)
+        h_out.copy_(d_out.view(src_t.dtype), non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = t.item()
+    return {"value": round(2 * nbytes * world * steps / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps,
+            "path": "pinned host -> H2D copy -> desc_transpose (C-ABI) -> D2H copy -> pinned host"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="8192f32")
+    ap.add_argument("--kernel", choices=["auto", "tma", "smem"], default="auto")
+    ap.add_argument("--oracle-seconds", type=float, default=12.0)
+    ap.add_argument("--reference-seconds", type=float, default=120.0)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    wl = dict(WORKLOADS[args.workload])
+    if args.impl == "reference":
+        return reference_arm(args, wl, world, rank)
+    return ours_arm(args, wl, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

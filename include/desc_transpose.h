@@ -1,0 +1,137 @@
+/*
+ * desc_transpose.h -- C ABI of the B200-native tiled matrix transpose
+ * (the running example of "Descend: A Safe GPU Systems Programming Language",
+ * arxiv 2305.03448).
+ *
+ * Operation ("transpose a matrix", P:77 / Listing 2 P:90-105,
+ * caption P:108, view type P:539-540; full elementwise transpose per DESIGN.md
+ * reading R1):
+ *
+ *     out[b][j][i] = in[b][i][j]      0 <= b < batch, 0 <= i < rows, 0 <= j < cols
+ *
+ * Layout.  All counts, leading dimensions and strides are in ELEMENTS (int64).
+ *   in  : batch matrices, each rows x cols, row-major, row pitch ld_in >= cols,
+ *         matrix b starts at in + b*stride_in.
+ *   out : batch matrices, each cols x rows, row-major, row pitch ld_out >= rows,
+ *         matrix b starts at out + b*stride_out.
+ *   Elements are opaque cells of desc_dtype_size(dtype) bytes: the library never
+ *   converts, so every bit pattern (NaN payloads, -0.0, subnormals) is moved
+ *   bit-exactly (R4, R11).  Bytes of `out` outside the logical
+ *   cols x rows regions (padding columns, gaps between matrices) are never
+ *   written (R8).
+ *
+ * Ownership (P:90-91 `&` / `&uniq`; R9).
+ *   `in` is a shared, read-only borrow; `out` is a unique borrow until the
+ *   stream reaches the operation.  The byte ranges spanned by in and out must
+ *   not overlap (DESC_ERR_ALIAS); in-place transposition is not supported.
+ *   For batch > 1 the output matrices must be pairwise disjoint:
+ *   stride_out >= (cols-1)*ld_out + rows (the narrowing rule), else
+ *   DESC_ERR_SHAPE.  Input matrices may overlap (read-only).  Strides must be >= 0.
+ *   The caller owns both buffers; the library allocates no device memory and
+ *   keeps only a host-side, thread-safe cache of TMA descriptors.
+ *
+ * Memory space.
+ *   Both pointers must be device (or managed) memory of the CURRENT device
+ *   (cudaPointerGetAttributes), else DESC_ERR_MEMSPACE.  desc_transpose_host is
+ *   the one entry point that takes host buffers.
+ *
+ * Launch configuration.  Derived inside the library from the shape
+ *   and the device's SM count: the caller passes no grid or block sizes, so the
+ *   "shared assumptions" bug of P:278-299 cannot occur.
+ *
+ * Synchronisation and errors.  Device entry points are ASYNCHRONOUS on `stream`
+ *   (a cudaStream_t passed as void*; NULL = legacy default stream).  This
+ *   deviates from Descend's implicit host wait.  Argument errors return
+ *   before any launch; a failed launch returns DESC_ERR_CUDA.  Nothing is thrown
+ *   across the ABI.  desc_last_error() returns a thread-local message for the
+ *   last non-OK status of the calling thread.  Empty shapes (batch, rows or
+ *   cols == 0) are a successful no-op with no launch (R10).
+ */
+#ifndef DESC_TRANSPOSE_H
+#define DESC_TRANSPOSE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DESC_VERSION 100 /* 1.0.0 */
+
+typedef enum desc_status {
+    DESC_OK = 0,
+    DESC_ERR_NULL = 1,      /* a required pointer is NULL                          */
+    DESC_ERR_SHAPE = 2,     /* negative size, ld < extent, overlapping batch outputs,
+                               int64 overflow of an extent, unsupported geometry    */
+    DESC_ERR_DTYPE = 3,     /* unknown desc_dtype                                   */
+    DESC_ERR_ALIAS = 4,     /* in and out byte ranges overlap (&uniq)     */
+    DESC_ERR_MEMSPACE = 5,  /* pointer not device memory of the current device       */
+    DESC_ERR_CUDA = 6,      /* CUDA runtime/driver error (see desc_last_error)       */
+    DESC_ERR_KERNEL = 7     /* requested kernel variant cannot run these arguments   */
+} desc_status;
+
+typedef enum desc_dtype {
+    DESC_F32 = 0, DESC_F64 = 1, DESC_I32 = 2, DESC_I64 = 3,
+    DESC_F16 = 4, DESC_BF16 = 5, DESC_U8 = 6
+} desc_dtype;
+
+/* Kernel variants (desc_transpose_ex).  AUTO picks TMA when the alignment rules
+ * below hold, else SMEM.
+ *   DESC_KERNEL_SMEM : 32x32 shared-memory tile, padded [32][33], 32x8 threads,
+ *                      predicated edges -- the corrected Listing 1 schedule
+ *                      (P:49-60 with the P:44 fix).  Any alignment.
+ *   DESC_KERNEL_TMA  : persistent, warp-specialised: TMA (cp.async.bulk.tensor)
+ *                      loads of 128-byte-swizzled tiles into a multi-stage
+ *                      mbarrier ring, conflict-free 16-byte shared reads,
+ *                      register micro-transposes, 16-byte coalesced stores.
+ *                      Needs 16-byte aligned in/out bases and ld*size,
+ *                      stride*size multiples of 16 bytes (when batch > 1);
+ *                      element size 1, 2, 4 or 8.                              */
+typedef enum desc_kernel {
+    DESC_KERNEL_AUTO = 0,
+    DESC_KERNEL_SMEM = 1,
+    DESC_KERNEL_TMA = 2
+} desc_kernel;
+
+/* Single transpose: in (rows x cols, pitch ld_in) -> out (cols x rows, pitch ld_out). */
+desc_status desc_transpose(const void *in, void *out, int64_t rows, int64_t cols,
+                           int64_t ld_in, int64_t ld_out, desc_dtype dtype,
+                           void *stream);
+
+/* Batched: `batch` independent transposes (layout above). */
+desc_status desc_transpose_batched(const void *in, void *out, int64_t batch,
+                                   int64_t rows, int64_t cols, int64_t ld_in,
+                                   int64_t ld_out, int64_t stride_in,
+                                   int64_t stride_out, desc_dtype dtype,
+                                   void *stream);
+
+/* Batched with an explicit kernel variant (tests / A-B measurement).  Returns
+ * DESC_ERR_KERNEL if the variant's alignment rules do not hold. */
+desc_status desc_transpose_ex(const void *in, void *out, int64_t batch,
+                              int64_t rows, int64_t cols, int64_t ld_in,
+                              int64_t ld_out, int64_t stride_in,
+                              int64_t stride_out, desc_dtype dtype,
+                              desc_kernel kernel, void *stream);
+
+/* The variant AUTO would run for these arguments (no launch, no pointer
+ * checks beyond alignment).  Returns DESC_KERNEL_SMEM or DESC_KERNEL_TMA. */
+desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
+                               int64_t rows, int64_t cols, int64_t ld_in,
+                               int64_t ld_out, int64_t stride_in,
+                               int64_t stride_out, desc_dtype dtype);
+
+/* Number of kernel launches the last successful device call of this thread
+ * issued (0 for an empty shape, 1 otherwise). */
+int desc_last_launch_count(void);
+
+const char *desc_status_string(desc_status s);
+const char *desc_last_error(void);
+size_t desc_dtype_size(desc_dtype t);
+int desc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DESC_TRANSPOSE_H */

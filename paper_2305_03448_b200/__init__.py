@@ -1,0 +1,199 @@
+"""paper_2305_03448_b200 -- B200-native tiled matrix transpose (Descend, arxiv 2305.03448).
+
+Thin Python binding over the C-ABI library libdesc_transpose.so
+(include/desc_transpose.h).  Argument marshalling only: every byte of the
+transpose is moved by the library's CUDA kernels.  There is NO CPU fallback:
+if the library is missing, every call raises.
+
+Raw entry points (same names and argument order as the C header):
+    desc_transpose, desc_transpose_batched, desc_transpose_ex, desc_select_kernel
+Tensor conveniences:
+    transpose(x, out=None, kernel="auto")          2-D, out = x^T
+    transpose_batched(x, out=None, kernel="auto")  3-D, transposes the last two dims
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "DescError", "DTYPE", "KERNEL", "lib_path", "load",
+    "desc_transpose", "desc_transpose_batched", "desc_transpose_ex", "desc_select_kernel",
+    "desc_status_string", "desc_last_error", "desc_dtype_size", "desc_version",
+    "desc_last_launch_count", "transpose", "transpose_batched",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_PKG, "libdesc_transpose.so")
+
+# enums (include/desc_transpose.h)
+STATUS = {0: "DESC_OK", 1: "DESC_ERR_NULL", 2: "DESC_ERR_SHAPE", 3: "DESC_ERR_DTYPE",
+          4: "DESC_ERR_ALIAS", 5: "DESC_ERR_MEMSPACE", 6: "DESC_ERR_CUDA", 7: "DESC_ERR_KERNEL"}
+DTYPE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3, "f16": 4, "bf16": 5, "u8": 6}
+KERNEL = {"auto": 0, "smem": 1, "tma": 2}
+KERNEL_NAME = {v: k for k, v in KERNEL.items()}
+
+_lib = None
+
+
+class DescError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.status_name = STATUS.get(status, f"status {status}")
+        super().__init__(f"{self.status_name}: {message}")
+
+
+def load():
+    """Load libdesc_transpose.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        raise RuntimeError(
+            f"{lib_path} is missing: build it with `python -m paper_2305_03448_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(lib_path)
+    i64, vp, ci = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+    lib.desc_transpose.argtypes = [vp, vp, i64, i64, i64, i64, ci, vp]
+    lib.desc_transpose.restype = ci
+    lib.desc_transpose_batched.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci, vp]
+    lib.desc_transpose_batched.restype = ci
+    lib.desc_transpose_ex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci, ci, vp]
+    lib.desc_transpose_ex.restype = ci
+    lib.desc_select_kernel.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci]
+    lib.desc_select_kernel.restype = ci
+    lib.desc_last_launch_count.argtypes = []
+    lib.desc_last_launch_count.restype = ci
+    lib.desc_status_string.argtypes = [ci]
+    lib.desc_status_string.restype = ctypes.c_char_p
+    lib.desc_last_error.argtypes = []
+    lib.desc_last_error.restype = ctypes.c_char_p
+    lib.desc_dtype_size.argtypes = [ci]
+    lib.desc_dtype_size.restype = ctypes.c_size_t
+    lib.desc_version.argtypes = []
+    lib.desc_version.restype = ci
+    _lib = lib
+    return lib
+
+
+def _check(status: int) -> int:
+    if status != 0:
+        raise DescError(status, load().desc_last_error().decode())
+    return status
+
+
+# ---- raw C-ABI wrappers (same names as the header) --------------------------------
+def desc_transpose(in_ptr, out_ptr, rows, cols, ld_in, ld_out, dtype, stream=0):
+    return _check(load().desc_transpose(in_ptr, out_ptr, rows, cols, ld_in, ld_out,
+                                        _dt(dtype), stream))
+
+
+def desc_transpose_batched(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride_in,
+                           stride_out, dtype, stream=0):
+    return _check(load().desc_transpose_batched(in_ptr, out_ptr, batch, rows, cols, ld_in,
+                                                ld_out, stride_in, stride_out, _dt(dtype),
+                                                stream))
+
+
+def desc_transpose_ex(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
+                      dtype, kernel="auto", stream=0):
+    return _check(load().desc_transpose_ex(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out,
+                                           stride_in, stride_out, _dt(dtype), _kn(kernel),
+                                           stream))
+
+
+def desc_select_kernel(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride_in,
+                       stride_out, dtype) -> str:
+    k = load().desc_select_kernel(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out,
+                                  stride_in, stride_out, _dt(dtype))
+    return KERNEL_NAME[k]
+
+
+def desc_status_string(status: int) -> str:
+    return load().desc_status_string(status).decode()
+
+
+def desc_last_error() -> str:
+    return load().desc_last_error().decode()
+
+
+def desc_dtype_size(dtype) -> int:
+    return load().desc_dtype_size(_dt(dtype))
+
+
+def desc_version() -> int:
+    return load().desc_version()
+
+
+def desc_last_launch_count() -> int:
+    return load().desc_last_launch_count()
+
+
+def _dt(dtype) -> int:
+    if isinstance(dtype, int):
+        return dtype
+    if isinstance(dtype, str):
+        return DTYPE[dtype]
+    return DTYPE[torch_dtype_name(dtype)]
+
+
+def _kn(kernel) -> int:
+    return kernel if isinstance(kernel, int) else KERNEL[kernel]
+
+
+# ---- torch tensor conveniences -------------------------------------------------------
+def torch_dtype_name(dt) -> str:
+    import torch
+    table = {torch.float32: "f32", torch.float64: "f64", torch.int32: "i32",
+             torch.int64: "i64", torch.float16: "f16", torch.bfloat16: "bf16",
+             torch.uint8: "u8", torch.int8: "u8", torch.bool: "u8",
+             torch.uint32: "i32", torch.uint64: "i64", torch.int16: "f16",
+             torch.uint16: "f16"}
+    if dt not in table:
+        raise DescError(3, f"unsupported torch dtype {dt}")
+    return table[dt]
+
+
+def _stream_of(t):
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def transpose(x, out=None, kernel: str = "auto"):
+    """out = x^T for a 2-D CUDA tensor with unit column stride (row pitch = x.stride(0))."""
+    import torch
+    if x.dim() != 2:
+        raise ValueError("transpose expects a 2-D tensor")
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty((cols, rows), dtype=x.dtype, device=x.device)
+    if tuple(out.shape) != (cols, rows) or out.dtype != x.dtype:
+        raise ValueError(f"out must be {(cols, rows)} {x.dtype}")
+    if rows and cols and (x.stride(1) != 1 or out.stride(1) != 1):
+        raise ValueError("tensors need unit stride in the last dimension")
+    ld_in = x.stride(0) if rows > 1 else cols
+    ld_out = out.stride(0) if cols > 1 else rows
+    desc_transpose_ex(x.data_ptr(), out.data_ptr(), 1, rows, cols, ld_in, ld_out, 0, 0,
+                      x.dtype, kernel, _stream_of(x))
+    return out
+
+
+def transpose_batched(x, out=None, kernel: str = "auto"):
+    """out[b] = x[b]^T for a 3-D CUDA tensor (unit stride in the last dimension)."""
+    import torch
+    if x.dim() != 3:
+        raise ValueError("transpose_batched expects a 3-D tensor")
+    batch, rows, cols = x.shape
+    if out is None:
+        out = torch.empty((batch, cols, rows), dtype=x.dtype, device=x.device)
+    if tuple(out.shape) != (batch, cols, rows) or out.dtype != x.dtype:
+        raise ValueError(f"out must be {(batch, cols, rows)} {x.dtype}")
+    if batch and rows and cols and (x.stride(2) != 1 or out.stride(2) != 1):
+        raise ValueError("tensors need unit stride in the last dimension")
+    ld_in = x.stride(1) if rows > 1 else cols
+    ld_out = out.stride(1) if cols > 1 else rows
+    stride_in = x.stride(0) if batch > 1 else 0
+    stride_out = out.stride(0) if batch > 1 else 0
+    desc_transpose_ex(x.data_ptr(), out.data_ptr(), batch, rows, cols, ld_in, ld_out,
+                      stride_in, stride_out, x.dtype, kernel, _stream_of(x))
+    return out

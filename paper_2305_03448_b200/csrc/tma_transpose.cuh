@@ -1,0 +1,240 @@
+// tma_transpose.cuh -- persistent, warp-specialised TMA transpose for sm_100a.
+//
+// Paper mapping (Listing 2):
+//   a2 tiling / CTA schedule  : `group_by_tile` + `sched(Y,X) block in grid` become a
+//                               persistent tile loop (tile t = blockIdx.x + k*gridDim.x)
+//   a3 tile-grid transpose    : the CTA that reads input tile (I,J) writes output tile (J,I)
+//   a4 load global->shared    : ONE TMA box load (cp.async.bulk.tensor) per 128-byte column
+//                               slice of the tile, 128-byte swizzle, into an S-stage ring
+//   a5 barrier ("sync"): mbarrier complete_tx (full) / consumer arrive (empty) --
+//                               the "synchronization releases borrows" rule
+//   a6 intra-tile transpose   : each lane reads VEC rows x 16 bytes with conflict-free
+//                               ld.shared.v4, transposes VEC x VEC in registers (renaming /
+//                               PRMT), and writes VEC coalesced 16-byte output rows
+//   a7 edges                  : TMA zero-fills out-of-range loads; stores are predicated
+//   a8 batch                  : third tensor-map dimension
+//
+// Shared-memory layout of one box: [TR rows][128 bytes], 16-byte chunk c of row r stored
+// at chunk c ^ (r & 7) (CU_TENSOR_MAP_SWIZZLE_128B; box base 1024-byte aligned).
+//
+// Lane -> micro-block map (conflict-free for every element size):
+//   VEC = 16/ES elements per chunk.  A lane owns the VEC x VEC micro-block at rows
+//   VEC*a .. VEC*a+VEC-1, chunk b.  lane bits [0, BB) -> low bits of b, [BB, 3) -> low bits
+//   of a, [3, 5) -> high bits of a, with BB = min(log2 VEC, 3).  In every 8-lane phase of a
+//   ld.shared.v4 the physical chunks b ^ ((VEC*a+k) & 7) are all distinct.
+#pragma once
+#include <cstdint>
+#include <utility>
+#include <cuda.h>
+
+#include "ptx.cuh"
+
+namespace desc {
+
+struct TmaParams {
+    void *out;
+    int64_t ld_out;      // elements
+    int64_t stride_out;  // elements
+    int32_t rows, cols, batch;
+    int32_t tiles_r, tiles_c;
+    int32_t rank3;       // 1 => 3-D tensor map (batch > 1)
+    int64_t ntiles;
+};
+
+template <int ES>
+struct TmaTraits {
+    static constexpr int VEC = 16 / ES;                       // elements per 16-byte chunk
+    static constexpr int LOGVEC = (VEC == 16) ? 4 : (VEC == 8) ? 3 : (VEC == 4) ? 2 : 1;
+    static constexpr int BB = LOGVEC < 3 ? LOGVEC : 3;         // lane bits selecting chunk
+    static constexpr int CHUNKS_PER_WARP = 1 << BB;
+    static constexpr int A_PER_WARP = 1 << (5 - BB);           // micro-row groups per warp
+    static constexpr int ROWS_PER_WARP = A_PER_WARP * VEC;     // input rows a warp covers
+    static constexpr int TC = 128 / ES;                        // columns of one swizzled box
+};
+
+// VEC x VEC register micro-transpose: r[k] = input row k (16 bytes), returns output row j.
+template <int ES, int J>
+__device__ __forceinline__ uint4 micro_row(const uint4 (&r)[16 / ES]) {
+    uint4 o;
+    if constexpr (ES == 4) {
+        const uint32_t *c0 = &r[0].x, *c1 = &r[1].x, *c2 = &r[2].x, *c3 = &r[3].x;
+        o.x = c0[J]; o.y = c1[J]; o.z = c2[J]; o.w = c3[J];
+    } else if constexpr (ES == 8) {
+        const uint32_t *c0 = &r[0].x, *c1 = &r[1].x;
+        o.x = c0[2 * J]; o.y = c0[2 * J + 1]; o.z = c1[2 * J]; o.w = c1[2 * J + 1];
+    } else if constexpr (ES == 2) {
+        constexpr uint32_t sel = (J & 1) ? 0x7632u : 0x5410u;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t a = (&r[2 * q].x)[J / 2];
+            const uint32_t b = (&r[2 * q + 1].x)[J / 2];
+            w[q] = __byte_perm(a, b, sel);
+        }
+        o = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {  // ES == 1
+        constexpr uint32_t byte = J & 3;
+        constexpr uint32_t sel2 = byte | ((4 + byte) << 4);   // bytes {a.byte, b.byte} -> [0,1]
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t lo = __byte_perm((&r[4 * q + 0].x)[J / 4], (&r[4 * q + 1].x)[J / 4], sel2);
+            const uint32_t hi = __byte_perm((&r[4 * q + 2].x)[J / 4], (&r[4 * q + 3].x)[J / 4], sel2);
+            w[q] = __byte_perm(lo, hi, 0x5410u);
+        }
+        o = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    return o;
+}
+
+template <int ES>
+__device__ __forceinline__ void store_partial(char *dst, const uint4 &v, int n) {
+    const char *s = reinterpret_cast<const char *>(&v);
+#pragma unroll
+    for (int e = 0; e < 16 / ES; ++e) {
+        if (e < n) {
+            if constexpr (ES == 8) *reinterpret_cast<uint64_t *>(dst + 8 * e) = *reinterpret_cast<const uint64_t *>(s + 8 * e);
+            else if constexpr (ES == 4) *reinterpret_cast<uint32_t *>(dst + 4 * e) = *reinterpret_cast<const uint32_t *>(s + 4 * e);
+            else if constexpr (ES == 2) *reinterpret_cast<uint16_t *>(dst + 2 * e) = *reinterpret_cast<const uint16_t *>(s + 2 * e);
+            else dst[e] = s[e];
+        }
+    }
+}
+
+template <int J, int ES>
+__device__ __forceinline__ void emit_row(const uint4 (&r)[16 / ES], char *out, int64_t ld_out_b,
+                                         int64_t orow0, int cols, int nvalid) {
+    constexpr int VEC = 16 / ES;
+    const int64_t orow = orow0 + J;
+    if (orow < cols) {
+        const uint4 o = micro_row<ES, J>(r);
+        char *p = out + orow * ld_out_b;
+        if (nvalid >= VEC) ptx::stg128(p, o);
+        else store_partial<ES>(p, o, nvalid);
+    }
+}
+
+template <int ES, int... J>
+__device__ __forceinline__ void emit_rows(const uint4 (&r)[16 / ES], char *out, int64_t ld_out_b,
+                                          int64_t orow0, int cols, int nvalid,
+                                          std::integer_sequence<int, J...>) {
+    (emit_row<J, ES>(r, out, ld_out_b, orow0, cols, nvalid), ...);
+}
+
+// TR: input rows per tile; NB: 128-byte column boxes per tile; STAGES: ring depth.
+template <int ES, int TR, int NB, int STAGES>
+struct TmaConfig {
+    using T = TmaTraits<ES>;
+    static constexpr int BOX_BYTES = TR * 128;
+    static constexpr int STAGE_BYTES = BOX_BYTES * NB;
+    static constexpr int TASKS_PER_BOX = (TR / T::ROWS_PER_WARP) * (8 / T::CHUNKS_PER_WARP);
+    static constexpr int TASKS = TASKS_PER_BOX * NB;
+    static constexpr int CONSUMERS = TASKS;          // one warp-task per consumer warp per tile
+    static constexpr int THREADS = 32 * (1 + CONSUMERS);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // +1024 for alignment
+    static constexpr int TILE_COLS = NB * T::TC;
+    static_assert(TR % T::ROWS_PER_WARP == 0, "TR must cover whole warp tasks");
+    static_assert(TR <= 256, "TMA box dimension <= 256");
+};
+
+template <int ES, int TR, int NB, int STAGES>
+__global__ void __launch_bounds__(TmaConfig<ES, TR, NB, STAGES>::THREADS)
+transpose_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaParams p) {
+    using C = TmaConfig<ES, TR, NB, STAGES>;
+    using T = TmaTraits<ES>;
+    constexpr int VEC = T::VEC;
+
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[STAGES];
+    __shared__ __align__(8) uint64_t empty_bar[STAGES];
+
+    const uint32_t smem_base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(ptx::smem_u32(&full_bar[s]), 1);
+            ptx::mbar_init(ptx::smem_u32(&empty_bar[s]), C::CONSUMERS);
+        }
+        ptx::fence_mbarrier_init();
+    }
+    __syncthreads();
+
+    const int64_t tiles_per_mat = (int64_t)p.tiles_r * p.tiles_c;
+
+    if (warp == 0) {
+        // ------------------------------ producer: one elected lane issues TMA
+        if (lane == 0) {
+            ptx::prefetch_tensormap(&map);
+            const uint64_t policy = ptx::policy_evict_first();
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+                const int s = it % STAGES;
+                const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+                ptx::mbar_wait(ptx::smem_u32(&empty_bar[s]), ph ^ 1u);   // slot released
+                const int64_t bt = t / tiles_per_mat;
+                const int64_t rem = t - bt * tiles_per_mat;
+                const int32_t ti = (int32_t)(rem / p.tiles_c);
+                const int32_t tj = (int32_t)(rem - (int64_t)ti * p.tiles_c);
+                const uint32_t fb = ptx::smem_u32(&full_bar[s]);
+                ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    const uint32_t dst = smem_base + s * C::STAGE_BYTES + nb * C::BOX_BYTES;
+                    const int32_t c0 = tj * C::TILE_COLS + nb * T::TC;
+                    if (p.rank3) ptx::tma_load_3d(dst, &map, fb, c0, ti * TR, (int32_t)bt, policy);
+                    else ptx::tma_load_2d(dst, &map, fb, c0, ti * TR, policy);
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------ consumers: smem -> registers -> global
+    const int cw = warp - 1;                         // consumer warp id == task id
+    const int box = cw / C::TASKS_PER_BOX;
+    const int tib = cw - box * C::TASKS_PER_BOX;
+    constexpr int CHUNK_GROUPS = 8 / T::CHUNKS_PER_WARP;
+    const int rgrp = tib / CHUNK_GROUPS;             // which ROWS_PER_WARP band of the box
+    const int cgrp = tib - rgrp * CHUNK_GROUPS;      // which chunk group
+    const int b = cgrp * T::CHUNKS_PER_WARP + (lane & ((1 << T::BB) - 1));
+    const int a_lo = (lane >> T::BB) & ((1 << (3 - T::BB)) - 1);
+    const int a_hi = lane >> 3;
+    const int a = rgrp * T::A_PER_WARP + a_hi * (1 << (3 - T::BB)) + a_lo;   // micro-row index
+    const int row_in_box = VEC * a;                  // first of this lane's VEC rows
+    const int64_t ld_out_b = p.ld_out * ES;
+
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+        const int64_t bt = t / tiles_per_mat;
+        const int64_t rem = t - bt * tiles_per_mat;
+        const int32_t ti = (int32_t)(rem / p.tiles_c);
+        const int32_t tj = (int32_t)(rem - (int64_t)ti * p.tiles_c);
+
+        ptx::mbar_wait(ptx::smem_u32(&full_bar[s]), ph);           // TMA bytes landed
+
+        const uint32_t bbase = smem_base + s * C::STAGE_BYTES + box * C::BOX_BYTES;
+        uint4 r[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            const int row = row_in_box + k;
+            r[k] = ptx::lds128(bbase + row * 128 + ((b ^ (row & 7)) << 4));
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty_bar[s]));   // release slot
+
+        const int64_t in_row0 = (int64_t)ti * TR + row_in_box;          // = output column
+        const int nvalid = (int)((int64_t)p.rows - in_row0 < VEC ? (int64_t)p.rows - in_row0 : VEC);
+        if (nvalid > 0) {
+            const int64_t orow0 = (int64_t)tj * C::TILE_COLS + box * T::TC + VEC * b;
+            char *out = reinterpret_cast<char *>(p.out) + (bt * p.stride_out + in_row0) * ES;
+            emit_rows<ES>(r, out, ld_out_b, orow0, p.cols, nvalid,
+                          std::make_integer_sequence<int, VEC>{});
+        }
+    }
+}
+
+}  // namespace desc

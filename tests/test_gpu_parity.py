@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, byte for byte.
+
+Bit-exact is the only bar (R14: a transpose moves bits, no tolerance).
+Every kernel variant reachable by dispatch is run, plus each variant forced.  Outputs
+live inside guard bands and padded rows filled with a sentinel, which must survive.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2305_03448_b200 as desc
+from paper_2305_03448_b200 import build as desc_build
+
+pytestmark = pytest.mark.gpu
+
+GUARD = 4096  # bytes of sentinel before and after every output buffer
+SENT = 0xA5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    desc_build.build()
+    desc.load()
+    torch.cuda.set_device(0)
+
+
+DT_OF_ES = {1: "u8", 2: "f16", 4: "f32", 8: "f64"}
+TORCH_INT = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
+NP_INT = {1: np.uint8, 2: np.int16, 4: np.int32, 8: np.int64}
+
+
+def _to_dev_bytes(a: np.ndarray, extra_front: int = 0) -> torch.Tensor:
+    """Copy raw bytes of `a` to a fresh uint8 device buffer at byte offset extra_front
+    (the buffer base itself is 256-byte aligned)."""
+    raw = np.frombuffer(a.tobytes(), dtype=np.uint8)
+    buf = torch.empty(raw.size + extra_front + 64, dtype=torch.uint8, device="cuda")
+    buf[extra_front:extra_front + raw.size] = torch.from_numpy(raw.copy()).cuda()
+    return buf
+
+
+def run_case(batch, rows, cols, es, kernel="auto", ld_in=None, ld_out=None, stride_in=None,
+             stride_out=None, in_off=0, out_off=0, src=None, check=True):
+    """Transpose a seeded input through desc_transpose_ex and compare with the oracle.
+    Returns the kernel AUTO would select."""
+    ld_in = cols if ld_in is None else ld_in
+    ld_out = rows if ld_out is None else ld_out
+    stride_in = rows * ld_in if stride_in is None else stride_in
+    stride_out = cols * ld_out if stride_out is None else stride_out
+    ut = synth.UINT_OF_SIZE[es]
+    n_in = (batch - 1) * stride_in + (rows - 1) * ld_in + cols if batch and rows and cols else 0
+    n_out = (batch - 1) * stride_out + (cols - 1) * ld_out + rows if batch and rows and cols else 0
+    inbuf = synth.random_bits((max(n_in, 1),), es, 1234 + rows * 7 + cols)  # padding = noise
+    if src is None:
+        if synth.nbits(cols) + synth.nbits(rows) + (synth.nbits(batch) if batch > 1 else 0) <= 8 * es:
+            src = synth.self_describing(batch, rows, cols, es)
+        else:
+            src = synth.with_specials(synth.random_bits((batch, rows, cols), es, 77 + rows), es, 3)
+    for b in range(batch):
+        for i in range(rows):
+            base = b * stride_in + i * ld_in
+            inbuf[base:base + cols] = src[b, i]
+    d_in = _to_dev_bytes(inbuf, in_off)
+    out_bytes = max(n_out, 1) * es
+    d_out = torch.full((GUARD + out_bytes + GUARD + out_off,), SENT, dtype=torch.uint8, device="cuda")
+    p_in = d_in.data_ptr() + in_off
+    p_out = d_out.data_ptr() + GUARD + out_off
+    sel = desc.desc_select_kernel(p_in, p_out, batch, rows, cols, ld_in, ld_out, stride_in,
+                                  stride_out, DT_OF_ES[es])
+    desc.desc_transpose_ex(p_in, p_out, batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
+                           DT_OF_ES[es], kernel, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    if not check:
+        return sel
+    host = d_out.cpu().numpy()
+    assert (host[:GUARD + out_off] == SENT).all(), "front guard band written"
+    assert (host[GUARD + out_off + out_bytes:] == SENT).all(), "back guard band written"
+    body = host[GUARD + out_off:GUARD + out_off + out_bytes].view(ut)
+    # expected: oracle into a sentinel-filled buffer of the same layout
+    exp = np.frombuffer(bytes([SENT]) * out_bytes, dtype=ut).copy()
+    if n_out:
+        oracle.transpose_raw(np.ascontiguousarray(src), exp, batch, rows, cols, cols, ld_out,
+                             rows * cols, stride_out, es)
+    if body.tobytes() != exp.tobytes():
+        bad = np.nonzero(body != exp)[0]
+        raise AssertionError(f"{bad.size} mismatching elements, first at flat {bad[:8]}")
+    return sel
+
+
+KERNELS = ["auto", "smem", "tma"]
+
+
+def _kernels_for(es, rows, cols, ld_in, ld_out):
+    ks = ["auto", "smem"]
+    if (ld_in * es) % 16 == 0 and (ld_out * es) % 16 == 0:
+        ks.append("tma")
+    return ks
+
+
+# --------------------------------------------------------------- small exhaustive-ish
+@pytest.mark.parametrize("es", [4, 8])
+def test_small_shapes_all_kernels(es):
+    """(rows, cols) over [1,40]^2 (every 3rd) with ld padded to 16-byte multiples so the
+    TMA path is eligible; every kernel variant."""
+    v = 16 // es
+    for rows in range(1, 41, 3):
+        for cols in range(1, 41, 3):
+            ld_in = -(-cols // v) * v
+            ld_out = -(-rows // v) * v
+            for k in _kernels_for(es, rows, cols, ld_in, ld_out):
+                run_case(1, rows, cols, es, k, ld_in=ld_in, ld_out=ld_out)
+
+
+@pytest.mark.parametrize("es", [1, 2, 4, 8])
+@pytest.mark.parametrize("n", [31, 32, 33, 63, 64, 65, 127, 128, 129])
+def test_edge_set(es, n):
+    v = 16 // es
+    for m in (31, 64, 129, 257):
+        for rows, cols in ((n, m), (m, n)):
+            ld_in = -(-cols // v) * v
+            ld_out = -(-rows // v) * v
+            for k in _kernels_for(es, rows, cols, ld_in, ld_out):
+                run_case(1, rows, cols, es, k, ld_in=ld_in, ld_out=ld_out)
+
+
+@pytest.mark.parametrize("es", [4, 8])
+def test_tight_ld_odd_shapes_fall_back(es):
+    """Tight ld that is not a 16-byte multiple: AUTO must pick the SMEM kernel and be exact."""
+    assert run_case(1, 67, 131, es) == "smem"
+    assert run_case(1, 3, 5, es) == "smem"
+
+
+@pytest.mark.parametrize("es", [4, 8])
+def test_padded_ld_guard_bands(es):
+    """T4: 67x131 with ld_in=136, ld_out=72: padding columns and guard bands untouched."""
+    for k in ("auto", "tma", "smem"):
+        run_case(1, 67, 131, es, k, ld_in=136, ld_out=72)
+
+
+@pytest.mark.parametrize("es", [4, 8])
+def test_misaligned_base(es):
+    """Base offsets that break 16-byte alignment route to the SMEM kernel and stay exact."""
+    assert run_case(1, 100, 200, es, in_off=es) == "smem"
+    assert run_case(1, 100, 200, es, out_off=es) == "smem"
+    with pytest.raises(desc.DescError, match="DESC_ERR_KERNEL"):
+        run_case(1, 100, 200, es, "tma", in_off=es, check=False)
+
+
+@pytest.mark.parametrize("es", [4, 8])
+def test_batched_odd_strides(es):
+    """T7: 7 x (33 x 65) with strides that leave gaps; input strides overlapping allowed."""
+    v = 16 // es
+    for k in ("auto", "smem", "tma"):
+        run_case(7, 33, 65, es, k, ld_in=65 + (-65) % v, ld_out=40, stride_in=33 * 72 + v,
+                 stride_out=65 * 40 + 2 * v)
+    run_case(5, 20, 24, es, "smem", ld_in=24, ld_out=20, stride_in=24 * 10, stride_out=480)
+
+
+def test_involution_and_determinism():
+    x = torch.from_numpy(synth.random_bits((1000, 1536), 4, 3).view(np.int32)).cuda()
+    y1 = desc.transpose(x)
+    y2 = desc.transpose(x)
+    z = desc.transpose(y1)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.equal(z, x)
+
+
+def test_tensor_api_dtypes():
+    for dt in (torch.float32, torch.float64, torch.int32, torch.int64, torch.float16,
+               torch.bfloat16, torch.uint8):
+        es = torch.empty(0, dtype=dt).element_size()
+        a = synth.random_bits((96, 80), es, 9)
+        x = torch.from_numpy(a.view(NP_INT[es])).cuda().view(dt)
+        y = desc.transpose(x)
+        torch.cuda.synchronize()
+        got = y.view(TORCH_INT[es]).cpu().numpy().view(synth.UINT_OF_SIZE[es])
+        assert got.tobytes() == oracle.transpose(a).tobytes(), dt
+
+
+def test_memspace_rejects_host_pointer():
+    h = torch.empty((64, 64), dtype=torch.float32).pin_memory()
+    d = torch.empty((64, 64), dtype=torch.float32, device="cuda")
+    with pytest.raises(desc.DescError, match="DESC_ERR_MEMSPACE"):
+        desc.desc_transpose(h.data_ptr(), d.data_ptr(), 64, 64, 64, 64, "f32")
+    a = np.zeros(4096, dtype=np.float32)
+    with pytest.raises(desc.DescError, match="DESC_ERR_MEMSPACE"):
+        desc.desc_transpose(d.data_ptr(), a.ctypes.data, 64, 64, 64, 64, "f32")
+
+
+def test_empty_is_noop():
+    x = torch.empty((0, 17), dtype=torch.float32, device="cuda")
+    y = desc.transpose(x)
+    assert y.shape == (17, 0) and desc.desc_last_launch_count() == 0
+
+
+# ------------------------------------------------------------ BASELINE.json configs
+def test_config0_64x64_f64():
+    for k in KERNELS:
+        run_case(1, 64, 64, 8, k)
+
+
+def test_config1_2048_f64():
+    a = synth.random_bits((1, 2048, 2048), 8, synth.BASE_SEED + 1)
+    for k in KERNELS:
+        run_case(1, 2048, 2048, 8, k, src=a)
+
+
+def test_config2_8192_f32_and_i32():
+    a = synth.random_bits((1, 8192, 8192), 4, synth.BASE_SEED + 2)
+    x = torch.from_numpy(a[0].view(np.int32)).cuda()
+    ref = oracle.transpose(a[0])
+    for k in ("auto", "tma", "smem"):
+        for dt in (torch.float32, torch.int32):
+            y = desc.transpose(x.view(dt), kernel=k)
+            torch.cuda.synchronize()
+            assert y.view(torch.int32).cpu().numpy().view(np.uint32).tobytes() == ref.tobytes()
+
+
+def test_config3_3000x5000_f64_and_misaligned_ld():
+    a = synth.random_bits((1, 3000, 5000), 8, synth.BASE_SEED + 3)
+    assert run_case(1, 3000, 5000, 8, src=a) == "tma"
+    assert run_case(1, 3000, 5000, 8, ld_in=5001, src=a) == "smem"
+
+
+def test_config4_batched_256x1024sq_f32():
+    """256 x (1024 x 1024) f32: every matrix checked against the oracle (self-describing)."""
+    src = synth.self_describing(256, 1024, 1024, 4)
+    x = torch.from_numpy(src.view(np.int32)).cuda()
+    y = desc.transpose_batched(x)
+    torch.cuda.synchronize()
+    assert y.cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(src).tobytes()
+
+
+def test_config5_65536_f32_sampled():
+    """65536 x 65536 f32 (16 GiB in + 16 GiB out) in one launch, hash-filled on device;
+    sampled 64 x 64 blocks (corners, edges, random) checked against the oracle."""
+    n = 65536
+    seed = synth.BASE_SEED + 5
+    x = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    synth.hash_fill_torch(x, 0, 0, n, seed, chunk_rows=2048)
+    y = torch.empty_like(x)
+    desc.transpose(x, y)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(seed)
+    picks = [(0, 0), (n - 64, n - 64), (0, n - 64), (n - 64, 0)] + \
+        [tuple(int(v) for v in rng.integers(0, n - 64, 2)) for _ in range(12)]
+    for i0, j0 in picks:
+        ii, jj = np.meshgrid(np.arange(i0, i0 + 64), np.arange(j0, j0 + 64), indexing="ij")
+        blk = synth.hash_expected_np(ii, jj, n, seed, 4)           # in[i0:i0+64, j0:j0+64]
+        exp = oracle.transpose(blk)                               # -> out[j0:, i0:]
+        got = y[j0:j0 + 64, i0:i0 + 64].cpu().numpy().view(np.uint32)
+        assert got.tobytes() == exp.tobytes(), (i0, j0)
+    del x, y
+    torch.cuda.empty_cache()
