@@ -35,6 +35,9 @@ import synth  # noqa: E402  (seeded input generators only; no method arithmetic)
 
 METRIC = "transpose effective GB/s (read+write) and % of HBM peak at 1/2/4/8 B200"
 L2_BYTES = 126 * 1024 * 1024
+KERNEL_FN = {"tma_st": "desc::transpose_tma2_kernel (TMA load + TMA store)",
+             "tma": "desc::transpose_tma_kernel (TMA load + st.global)",
+             "smem": "desc::transpose_smem_kernel (32x33 smem tile)"}
 
 WORKLOADS = {
     "8192f32": dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4,
@@ -366,7 +369,7 @@ def ours_arm(args, wl, world, rank, local):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(args.workload), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes,
-                         "kernel": f"transpose_{selected}_kernel",
+                         "kernel": KERNEL_FN[selected],
                          "launch_ms_median": round(statistics.median(per_launch), 5),
                          "launch_ms_p10": round(float(np.percentile(per_launch, 10)), 5),
                          "launch_ms_p90": round(float(np.percentile(per_launch, 90)), 5),
@@ -428,7 +431,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="8192f32")
-    ap.add_argument("--kernel", choices=["auto", "tma", "smem"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem"], default="auto")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
     ap.add_argument("--reference-seconds", type=float, default=120.0)
     ap.add_argument("--e2e-steps", type=int, default=20)

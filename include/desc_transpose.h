@@ -76,8 +76,9 @@ typedef enum desc_dtype {
     DESC_F16 = 4, DESC_BF16 = 5, DESC_U8 = 6
 } desc_dtype;
 
-/* Kernel variants (desc_transpose_ex).  AUTO picks TMA when the alignment rules
- * below hold, else SMEM.
+/* Kernel variants (desc_transpose_ex).  AUTO picks TMA_ST when the alignment rules
+ * below hold and the element size is 4 or 8 with rows*size >= 16, else TMA when the
+ * alignment rules hold, else SMEM.
  *   DESC_KERNEL_SMEM : 32x32 shared-memory tile, padded [32][33], 32x8 threads,
  *                      predicated edges -- the corrected Listing 1 schedule
  *                      (P:49-60 with the P:44 fix).  Any alignment.
@@ -87,11 +88,16 @@ typedef enum desc_dtype {
  *                      register micro-transposes, 16-byte coalesced stores.
  *                      Needs 16-byte aligned in/out bases and ld*size,
  *                      stride*size multiples of 16 bytes (when batch > 1);
- *                      element size 1, 2, 4 or 8.                              */
+ *                      element size 1, 2, 4 or 8.
+ *   DESC_KERNEL_TMA_ST : as DESC_KERNEL_TMA, but the transposed tile is staged in
+ *                      128-byte-swizzled shared memory and written with TMA bulk
+ *                      tensor stores (cp.async.bulk.tensor shared->global).  Same
+ *                      alignment rules; element size 4 or 8.                    */
 typedef enum desc_kernel {
     DESC_KERNEL_AUTO = 0,
     DESC_KERNEL_SMEM = 1,
-    DESC_KERNEL_TMA = 2
+    DESC_KERNEL_TMA = 2,
+    DESC_KERNEL_TMA_ST = 3
 } desc_kernel;
 
 /* Single transpose: in (rows x cols, pitch ld_in) -> out (cols x rows, pitch ld_out). */
@@ -115,7 +121,7 @@ desc_status desc_transpose_ex(const void *in, void *out, int64_t batch,
                               desc_kernel kernel, void *stream);
 
 /* The variant AUTO would run for these arguments (no launch, no pointer
- * checks beyond alignment).  Returns DESC_KERNEL_SMEM or DESC_KERNEL_TMA. */
+ * checks beyond alignment).  Returns DESC_KERNEL_SMEM, _TMA or _TMA_ST. */
 desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
                                int64_t rows, int64_t cols, int64_t ld_in,
                                int64_t ld_out, int64_t stride_in,

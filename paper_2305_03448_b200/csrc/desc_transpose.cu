@@ -8,6 +8,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -16,6 +17,7 @@
 #include "../../include/desc_transpose.h"
 #include "smem_transpose.cuh"
 #include "tma_transpose.cuh"
+#include "tma_store_transpose.cuh"
 
 namespace {
 
@@ -108,29 +110,39 @@ desc_status get_encode(PFN_cuTensorMapEncodeTiled_v12000 *fn) {
     return DESC_OK;
 }
 
+// A 2-D (or batched 3-D) row-major matrix seen by TMA: `inner` elements per row (pitch
+// ld), `outer` rows, `batch` matrices (pitch stride); box = box_inner x box_outer.
 struct MapKey {
     uintptr_t ptr;
-    int64_t rows, cols, batch, ld, stride;
-    int es, box_rows;
+    int64_t inner, outer, batch, ld, stride;
+    int es, box_inner, box_outer;
     bool operator==(const MapKey &o) const {
-        return ptr == o.ptr && rows == o.rows && cols == o.cols && batch == o.batch &&
-               ld == o.ld && stride == o.stride && es == o.es && box_rows == o.box_rows;
+        return ptr == o.ptr && inner == o.inner && outer == o.outer && batch == o.batch &&
+               ld == o.ld && stride == o.stride && es == o.es && box_inner == o.box_inner &&
+               box_outer == o.box_outer;
     }
 };
 struct MapKeyHash {
     size_t operator()(const MapKey &k) const {
         size_t h = std::hash<uintptr_t>()(k.ptr);
         auto mix = [&h](int64_t v) { h ^= std::hash<int64_t>()(v) + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2); };
-        mix(k.rows); mix(k.cols); mix(k.batch); mix(k.ld); mix(k.stride); mix(k.es); mix(k.box_rows);
+        mix(k.inner); mix(k.outer); mix(k.batch); mix(k.ld); mix(k.stride); mix(k.es);
+        mix(k.box_inner); mix(k.box_outer);
         return h;
     }
 };
 std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
-desc_status tensor_map(const Args &a, int box_rows, CUtensorMap *out) {
-    MapKey key{reinterpret_cast<uintptr_t>(a.in), a.rows, a.cols, a.batch, a.ld_in,
-               a.stride_in, a.es, box_rows};
+CUtensorMapL2promotion promo() {
+    static const int v = [] { const char *e = getenv("DESC_TMA_PROMO"); return e ? atoi(e) : 2; }();
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+         : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
+// Encode (or fetch from the cache) a 128-byte-swizzled tiled tensor map.
+desc_status tensor_map(const MapKey &key, CUtensorMap *out) {
     {
         std::lock_guard<std::mutex> lk(g_map_mu);
         auto it = g_maps.find(key);
@@ -138,19 +150,19 @@ desc_status tensor_map(const Args &a, int box_rows, CUtensorMap *out) {
     }
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (desc_status s = get_encode(&encode)) return s;
-    CUtensorMapDataType dt = a.es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64
-                           : a.es == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
-                           : a.es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
-                                       : CU_TENSOR_MAP_DATA_TYPE_UINT8;
-    const cuuint32_t rank = a.batch > 1 ? 3 : 2;
-    cuuint64_t dims[3] = {(cuuint64_t)a.cols, (cuuint64_t)a.rows, (cuuint64_t)a.batch};
-    cuuint64_t strides[2] = {(cuuint64_t)(a.ld_in * a.es), (cuuint64_t)(a.stride_in * a.es)};
-    cuuint32_t box[3] = {(cuuint32_t)(128 / a.es), (cuuint32_t)box_rows, 1};
+    CUtensorMapDataType dt = key.es == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64
+                           : key.es == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                           : key.es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                         : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    const cuuint32_t rank = key.batch > 1 ? 3 : 2;
+    cuuint64_t dims[3] = {(cuuint64_t)key.inner, (cuuint64_t)key.outer, (cuuint64_t)key.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(key.ld * key.es), (cuuint64_t)(key.stride * key.es)};
+    cuuint32_t box[3] = {(cuuint32_t)key.box_inner, (cuuint32_t)key.box_outer, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMap m;
-    CUresult r = encode(&m, dt, rank, const_cast<void *>(a.in), dims, strides, box, estr,
+    CUresult r = encode(&m, dt, rank, reinterpret_cast<void *>(key.ptr), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(DESC_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
     std::lock_guard<std::mutex> lk(g_map_mu);
@@ -158,6 +170,19 @@ desc_status tensor_map(const Args &a, int box_rows, CUtensorMap *out) {
     g_maps.emplace(key, m);
     *out = m;
     return DESC_OK;
+}
+
+desc_status in_map(const Args &a, int box_rows, CUtensorMap *m) {
+    MapKey k{reinterpret_cast<uintptr_t>(a.in), a.cols, a.rows, a.batch, a.ld_in, a.stride_in,
+             a.es, 128 / a.es, box_rows};
+    return tensor_map(k, m);
+}
+
+desc_status out_map(const Args &a, int box_rows, CUtensorMap *m) {
+    const int64_t rows_main = a.rows - a.rows % (16 / a.es);   // 16-byte clipping granule
+    MapKey k{reinterpret_cast<uintptr_t>(a.out), rows_main, a.cols, a.batch, a.ld_out, a.stride_out,
+             a.es, 128 / a.es, box_rows};
+    return tensor_map(k, m);
 }
 
 // ---- TMA eligibility -------------------------------------------------------------
@@ -169,51 +194,103 @@ bool tma_eligible(const Args &a) {
     if (a.batch > 1 && a.stride_in == 0) return false;
     const int64_t lim = (int64_t)1 << 31;
     if (a.rows >= lim || a.cols >= lim || a.batch >= lim) return false;
-    if (a.ld_in * a.es >= ((int64_t)1 << 40) || a.stride_in * a.es >= ((int64_t)1 << 40)) return false;
+    const int64_t lim40 = (int64_t)1 << 40;
+    if (a.ld_in * a.es >= lim40 || a.stride_in * a.es >= lim40) return false;
+    if (a.ld_out * a.es >= lim40 || a.stride_out * a.es >= lim40) return false;
     return true;
 }
 
-// ---- launchers -----------------------------------------------------------------------
-template <int ES, int TR, int NB, int STAGES>
-desc_status launch_tma(const Args &a) {
-    using C = desc::TmaConfig<ES, TR, NB, STAGES>;
-    auto kern = desc::transpose_tma_kernel<ES, TR, NB, STAGES>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    });
-    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
+// Development knobs (read once; A/B measurement only).
+int dev_knob(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
 
+// Raster group (tile rows per group).  Default: the whole tile column (tiles walk down
+// the input's columns, so the tiles in flight write whole output rows contiguously);
+// measured best on 8192^2 f32 (gpurun_out/sweep_group2.txt: 90.6 us vs 92.6 us for
+// near-square windows).  DESC_TMA_GROUP=g forces g (A/B only).
+int tile_group(int grid, int tr, int tc, int tiles_r) {
+    (void)grid; (void)tr; (void)tc;
+    static const int forced = dev_knob("DESC_TMA_GROUP", 0);
+    int g = forced > 0 ? forced : tiles_r;
+    if (g > tiles_r) g = tiles_r;
+    return g < 1 ? 1 : g;
+}
+
+// The TMA-store kernel takes 4/8-byte cells whose output rows span >= one 16-byte chunk.
+bool tma_store_ok(const Args &a) { return (a.es == 4 || a.es == 8) && a.rows * a.es >= 16; }
+
+// ---- launchers -----------------------------------------------------------------------
+// Shared launch plumbing of the persistent TMA kernels: dynamic-smem opt-in (once per
+// kernel instantiation), grid = min(tiles, SMs x occupancy), tile raster parameters.
+template <typename Kern>
+desc_status tma_prepare(Kern kern, int threads, int smem, int tr, int tile_cols, const Args &a,
+                        desc::TmaParams *p, int *grid, cudaFuncAttributes *) {
+    static std::mutex mu;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    }
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     DevInfo di;
     if (desc_status s = device_info(dev, &di)) return s;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM_BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (occ < 1) occ = 1;
-
-    CUtensorMap map;
-    if (desc_status s = tensor_map(a, TR, &map)) return s;
-
-    desc::TmaParams p;
-    p.out = a.out;
-    p.ld_out = a.ld_out;
-    p.stride_out = a.stride_out;
-    p.rows = (int32_t)a.rows;
-    p.cols = (int32_t)a.cols;
-    p.batch = (int32_t)a.batch;
-    p.tiles_r = (int32_t)((a.rows + TR - 1) / TR);
-    p.tiles_c = (int32_t)((a.cols + C::TILE_COLS - 1) / C::TILE_COLS);
-    p.rank3 = a.batch > 1 ? 1 : 0;
-    p.ntiles = (int64_t)p.tiles_r * p.tiles_c * a.batch;
+    p->out = a.out;
+    p->ld_out = a.ld_out;
+    p->stride_out = a.stride_out;
+    p->rows = (int32_t)a.rows;
+    p->rows_main = (int32_t)(a.rows - a.rows % (16 / a.es));
+    p->cols = (int32_t)a.cols;
+    p->batch = (int32_t)a.batch;
+    p->tiles_r = (int32_t)((a.rows + tr - 1) / tr);
+    p->tiles_c = (int32_t)((a.cols + tile_cols - 1) / tile_cols);
+    p->rank3 = a.batch > 1 ? 1 : 0;
+    p->ntiles = (int64_t)p->tiles_r * p->tiles_c * a.batch;
     const int64_t max_grid = (int64_t)di.sms * occ;
-    const int grid = (int)(p.ntiles < max_grid ? p.ntiles : max_grid);
+    *grid = (int)(p->ntiles < max_grid ? p->ntiles : max_grid);
+    p->group = tile_group(*grid, tr, tile_cols, p->tiles_r);
+    p->evict_first = dev_knob("DESC_TMA_EVICT", 0);
+    return DESC_OK;
+}
+
+template <int ES, int TR, int NB, int STAGES, int CW>
+desc_status launch_tma(const Args &a) {
+    using C = desc::TmaConfig<ES, TR, NB, STAGES, CW>;
+    auto kern = desc::transpose_tma_kernel<ES, TR, NB, STAGES, CW>;
+    desc::TmaParams p;
+    int grid = 0;
+    if (desc_status s = tma_prepare(kern, C::THREADS, C::SMEM_BYTES, TR, C::TILE_COLS, a, &p, &grid, nullptr))
+        return s;
+    CUtensorMap map;
+    if (desc_status s = in_map(a, TR, &map)) return s;
     kern<<<grid, C::THREADS, C::SMEM_BYTES, a.stream>>>(map, p);
-    e = cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "transpose_tma_kernel launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
+template <int ES, int TR, int NB, int STAGES, int CW, int OBUF>
+desc_status launch_tma2(const Args &a) {
+    using C = desc::Tma2Config<ES, TR, NB, STAGES, CW, OBUF>;
+    auto kern = desc::transpose_tma2_kernel<ES, TR, NB, STAGES, CW, OBUF>;
+    desc::TmaParams p;
+    int grid = 0;
+    if (desc_status s = tma_prepare(kern, C::THREADS, C::SMEM_BYTES, TR, C::TILE_COLS, a, &p, &grid, nullptr))
+        return s;
+    CUtensorMap min, mout;
+    if (desc_status s = in_map(a, TR, &min)) return s;
+    if (desc_status s = out_map(a, C::TILE_COLS, &mout)) return s;
+    kern<<<grid, C::THREADS, C::SMEM_BYTES, a.stream>>>(min, mout, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "transpose_tma2_kernel launch");
     g_last_launches = 1;
     return DESC_OK;
 }
@@ -238,14 +315,89 @@ desc_status launch_smem(const Args &a) {
     return DESC_OK;
 }
 
+// Development knob: DESC_TMA_CFG=<n> selects a tile/pipeline configuration for A/B
+// measurement (read once).  The default (0) is the tuned configuration.
+int tma_cfg() {
+    static int cfg = [] {
+        const char *e = getenv("DESC_TMA_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    return cfg;
+}
+
 desc_status run_tma(const Args &a) {
+    const int cfg = tma_cfg();
     switch (a.es) {
-        case 4: return launch_tma<4, 128, 1, 4>(a);
-        case 8: return launch_tma<8, 128, 1, 4>(a);
-        case 2: return launch_tma<2, 128, 1, 4>(a);
-        case 1: return launch_tma<1, 128, 1, 4>(a);
+        case 4:
+            switch (cfg) {
+                case 1: return launch_tma<4, 64, 2, 4, 8>(a);
+                case 2: return launch_tma<4, 128, 2, 3, 8>(a);
+                case 3: return launch_tma<4, 256, 1, 3, 8>(a);
+                case 4: return launch_tma<4, 32, 4, 6, 8>(a);
+                case 5: return launch_tma<4, 128, 1, 8, 8>(a);
+                case 6: return launch_tma<4, 64, 1, 8, 4>(a);
+                case 7: return launch_tma<4, 64, 4, 3, 8>(a);
+                case 8: return launch_tma<4, 128, 1, 4, 4>(a);
+                default: return launch_tma<4, 128, 1, 4, 8>(a);
+            }
+        case 8:
+            switch (cfg) {
+                case 1: return launch_tma<8, 64, 2, 4, 8>(a);
+                case 2: return launch_tma<8, 128, 2, 3, 16>(a);
+                case 3: return launch_tma<8, 256, 1, 3, 16>(a);
+                case 4: return launch_tma<8, 32, 4, 6, 8>(a);
+                case 5: return launch_tma<8, 128, 1, 8, 16>(a);
+                case 6: return launch_tma<8, 64, 1, 8, 4>(a);
+                case 7: return launch_tma<8, 64, 4, 3, 16>(a);
+                case 8: return launch_tma<8, 128, 1, 4, 8>(a);
+                default: return launch_tma<8, 128, 1, 4, 16>(a);
+            }
+        case 2: return launch_tma<2, 128, 1, 4, 4>(a);
+        case 1: return launch_tma<1, 128, 1, 4, 2>(a);
     }
     return fail(DESC_ERR_DTYPE, "unsupported element size %d", a.es);
+}
+
+desc_status run_tma2(const Args &a) {
+    const int cfg = tma_cfg();
+    switch (a.es) {
+        case 4:
+            switch (cfg) {
+                case 1: return launch_tma2<4, 64, 2, 4, 8, 2>(a);
+                case 2: return launch_tma2<4, 128, 1, 3, 8, 3>(a);
+                case 3: return launch_tma2<4, 128, 1, 4, 4, 2>(a);
+                case 4: return launch_tma2<4, 64, 1, 6, 4, 3>(a);
+                case 5: return launch_tma2<4, 256, 1, 2, 8, 2>(a);
+                case 6: return launch_tma2<4, 256, 1, 3, 8, 2>(a);
+                case 7: return launch_tma2<4, 256, 1, 2, 16, 2>(a);
+                case 8: return launch_tma2<4, 256, 1, 4, 8, 2>(a);
+                case 9: return launch_tma2<4, 128, 2, 2, 8, 2>(a);
+                case 10: return launch_tma2<4, 256, 1, 2, 4, 2>(a);
+                case 11: return launch_tma2<4, 128, 1, 2, 8, 2>(a);
+                case 12: return launch_tma2<4, 128, 1, 4, 8, 2>(a);
+                // tuned (gpurun_out sweeps, profiles/): 128 x 64 tile, 2-stage ring,
+                // 2 output buffers, 8 consumer warps, 1 CTA (288 threads, 129 KB) per SM
+                default: return launch_tma2<4, 128, 2, 2, 8, 2>(a);
+            }
+        case 8:
+            switch (cfg) {
+                case 1: return launch_tma2<8, 64, 2, 4, 8, 2>(a);
+                case 2: return launch_tma2<8, 128, 1, 3, 16, 3>(a);
+                case 3: return launch_tma2<8, 128, 1, 4, 8, 2>(a);
+                case 4: return launch_tma2<8, 64, 1, 6, 8, 3>(a);
+                case 5: return launch_tma2<8, 128, 2, 2, 16, 2>(a);
+                case 6: return launch_tma2<8, 256, 1, 2, 16, 2>(a);
+                case 7: return launch_tma2<8, 256, 1, 3, 16, 2>(a);
+                case 8: return launch_tma2<8, 128, 1, 2, 16, 2>(a);
+                case 9: return launch_tma2<8, 256, 1, 2, 8, 2>(a);
+                case 10: return launch_tma2<8, 128, 2, 3, 16, 2>(a);
+                case 11: return launch_tma2<8, 64, 2, 2, 8, 2>(a);
+                case 12: return launch_tma2<8, 128, 1, 4, 16, 2>(a);
+                // tuned: 128 x 16 tile, 2-stage ring, 2 output buffers, 16 consumer warps
+                default: return launch_tma2<8, 128, 1, 2, 16, 2>(a);
+            }
+    }
+    return fail(DESC_ERR_KERNEL, "TMA-store kernel supports 4- and 8-byte elements only");
 }
 
 desc_status run_smem(const Args &a) {
@@ -321,7 +473,13 @@ desc_status run(const Args &a, desc_kernel k) {
     const bool tma_ok = tma_eligible(a);
     if (k == DESC_KERNEL_TMA && !tma_ok)
         return fail(DESC_ERR_KERNEL, "TMA kernel needs 16-byte aligned bases, ld*size and stride*size");
+    if (k == DESC_KERNEL_TMA_ST && !tma_ok)
+        return fail(DESC_ERR_KERNEL, "TMA kernels need 16-byte aligned bases, ld*size and stride*size");
+    if (k == DESC_KERNEL_TMA_ST && !tma_store_ok(a))
+        return fail(DESC_ERR_KERNEL, "TMA-store kernel needs 4/8-byte elements and rows*size >= 16");
+    if (k == DESC_KERNEL_TMA_ST) return run_tma2(a);
     if (k == DESC_KERNEL_SMEM || (k == DESC_KERNEL_AUTO && !tma_ok)) return run_smem(a);
+    if (k == DESC_KERNEL_AUTO && tma_store_ok(a)) return run_tma2(a);
     if (k == DESC_KERNEL_TMA || k == DESC_KERNEL_AUTO) return run_tma(a);
     return fail(DESC_ERR_KERNEL, "unknown kernel variant %d", (int)k);
 }
@@ -356,8 +514,8 @@ desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch, i
                                int64_t stride_out, desc_dtype dtype) {
     Args a{in, const_cast<void *>(out), batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
            dtype_size(dtype), nullptr};
-    if (a.es == 0) return DESC_KERNEL_SMEM;
-    return tma_eligible(a) ? DESC_KERNEL_TMA : DESC_KERNEL_SMEM;
+    if (a.es == 0 || !tma_eligible(a)) return DESC_KERNEL_SMEM;
+    return tma_store_ok(a) ? DESC_KERNEL_TMA_ST : DESC_KERNEL_TMA;
 }
 
 int desc_last_launch_count(void) { return g_last_launches; }

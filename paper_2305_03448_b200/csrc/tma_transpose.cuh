@@ -36,10 +36,37 @@ struct TmaParams {
     int64_t ld_out;      // elements
     int64_t stride_out;  // elements
     int32_t rows, cols, batch;
+    int32_t rows_main;   // rows rounded down to 16 bytes (TMA-store map extent)
     int32_t tiles_r, tiles_c;
     int32_t rank3;       // 1 => 3-D tensor map (batch > 1)
+    int32_t group;       // tile rows per raster group (>= 1), see tile_coords
+    int32_t evict_first; // 1 => L2 evict_first hint on the TMA loads
     int64_t ntiles;
 };
+
+// Linear tile id -> (matrix, tile row, tile col).  Tiles are rastered in groups of
+// `group` tile rows walked column by column, so the tiles in flight at any moment
+// (one per CTA) form a near-square window of the matrix: both the rows read and the
+// rows written are touched in long contiguous runs (DRAM page locality on both sides
+// of the transpose).
+struct TileCoord {
+    int64_t bt;
+    int32_t ti, tj;
+};
+__device__ __forceinline__ TileCoord tile_coords(int64_t t, const TmaParams &p) {
+    const int64_t per_mat = (int64_t)p.tiles_r * p.tiles_c;
+    TileCoord c;
+    c.bt = t / per_mat;
+    const int64_t rem = t - c.bt * per_mat;
+    const int64_t per_group = (int64_t)p.group * p.tiles_c;
+    const int32_t g = (int32_t)(rem / per_group);
+    const int32_t in_g = (int32_t)(rem - (int64_t)g * per_group);
+    const int32_t g0 = g * p.group;
+    const int32_t gsz = min(p.group, p.tiles_r - g0);
+    c.tj = in_g / gsz;
+    c.ti = g0 + (in_g - c.tj * gsz);
+    return c;
+}
 
 template <int ES>
 struct TmaTraits {
@@ -87,16 +114,27 @@ __device__ __forceinline__ uint4 micro_row(const uint4 (&r)[16 / ES]) {
     return o;
 }
 
+// 32-bit word w of a uint4 (w is a compile-time constant after unrolling).
+__device__ __forceinline__ uint32_t word(const uint4 &v, int w) {
+    return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+}
+
+// Store the first n (< 16/ES) elements of v at dst (edge micro-block, R6/R8).
 template <int ES>
 __device__ __forceinline__ void store_partial(char *dst, const uint4 &v, int n) {
-    const char *s = reinterpret_cast<const char *>(&v);
 #pragma unroll
     for (int e = 0; e < 16 / ES; ++e) {
         if (e < n) {
-            if constexpr (ES == 8) *reinterpret_cast<uint64_t *>(dst + 8 * e) = *reinterpret_cast<const uint64_t *>(s + 8 * e);
-            else if constexpr (ES == 4) *reinterpret_cast<uint32_t *>(dst + 4 * e) = *reinterpret_cast<const uint32_t *>(s + 4 * e);
-            else if constexpr (ES == 2) *reinterpret_cast<uint16_t *>(dst + 2 * e) = *reinterpret_cast<const uint16_t *>(s + 2 * e);
-            else dst[e] = s[e];
+            if constexpr (ES == 8) {
+                const uint64_t d = ((uint64_t)word(v, 2 * e + 1) << 32) | word(v, 2 * e);
+                *reinterpret_cast<uint64_t *>(dst + 8 * e) = d;
+            } else if constexpr (ES == 4) {
+                *reinterpret_cast<uint32_t *>(dst + 4 * e) = word(v, e);
+            } else if constexpr (ES == 2) {
+                *reinterpret_cast<uint16_t *>(dst + 2 * e) = (uint16_t)(word(v, e / 2) >> (16 * (e & 1)));
+            } else {
+                dst[e] = (char)(word(v, e / 4) >> (8 * (e & 3)));
+            }
         }
     }
 }
@@ -121,28 +159,34 @@ __device__ __forceinline__ void emit_rows(const uint4 (&r)[16 / ES], char *out, 
     (emit_row<J, ES>(r, out, ld_out_b, orow0, cols, nvalid), ...);
 }
 
-// TR: input rows per tile; NB: 128-byte column boxes per tile; STAGES: ring depth.
-template <int ES, int TR, int NB, int STAGES>
+// TR: input rows per tile; NB: 128-byte column boxes per tile; STAGES: ring depth;
+// CW: consumer warps (each handles TASKS/CW warp-tasks of every tile).
+template <int ES, int TR, int NB, int STAGES, int CW>
 struct TmaConfig {
     using T = TmaTraits<ES>;
     static constexpr int BOX_BYTES = TR * 128;
     static constexpr int STAGE_BYTES = BOX_BYTES * NB;
-    static constexpr int TASKS_PER_BOX = (TR / T::ROWS_PER_WARP) * (8 / T::CHUNKS_PER_WARP);
+    static constexpr int CHUNK_GROUPS = 8 / T::CHUNKS_PER_WARP;
+    static constexpr int TASKS_PER_BOX = (TR / T::ROWS_PER_WARP) * CHUNK_GROUPS;
     static constexpr int TASKS = TASKS_PER_BOX * NB;
-    static constexpr int CONSUMERS = TASKS;          // one warp-task per consumer warp per tile
+    static constexpr int CONSUMERS = CW;
+    static constexpr int TPW = TASKS / CW;           // warp-tasks per consumer warp per tile
     static constexpr int THREADS = 32 * (1 + CONSUMERS);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // +1024 for alignment
     static constexpr int TILE_COLS = NB * T::TC;
     static_assert(TR % T::ROWS_PER_WARP == 0, "TR must cover whole warp tasks");
+    static_assert(TASKS % CW == 0, "tasks must split evenly over consumer warps");
     static_assert(TR <= 256, "TMA box dimension <= 256");
+    static_assert(THREADS <= 1024, "block too large");
 };
 
-template <int ES, int TR, int NB, int STAGES>
-__global__ void __launch_bounds__(TmaConfig<ES, TR, NB, STAGES>::THREADS)
+template <int ES, int TR, int NB, int STAGES, int CW>
+__global__ void __launch_bounds__(TmaConfig<ES, TR, NB, STAGES, CW>::THREADS)
 transpose_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaParams p) {
-    using C = TmaConfig<ES, TR, NB, STAGES>;
+    using C = TmaConfig<ES, TR, NB, STAGES, CW>;
     using T = TmaTraits<ES>;
     constexpr int VEC = T::VEC;
+    constexpr int TPW = C::TPW;
 
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[STAGES];
@@ -161,22 +205,19 @@ transpose_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaParams p)
     }
     __syncthreads();
 
-    const int64_t tiles_per_mat = (int64_t)p.tiles_r * p.tiles_c;
-
     if (warp == 0) {
         // ------------------------------ producer: one elected lane issues TMA
         if (lane == 0) {
             ptx::prefetch_tensormap(&map);
-            const uint64_t policy = ptx::policy_evict_first();
+            const uint64_t policy = p.evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
             int it = 0;
             for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
                 ptx::mbar_wait(ptx::smem_u32(&empty_bar[s]), ph ^ 1u);   // slot released
-                const int64_t bt = t / tiles_per_mat;
-                const int64_t rem = t - bt * tiles_per_mat;
-                const int32_t ti = (int32_t)(rem / p.tiles_c);
-                const int32_t tj = (int32_t)(rem - (int64_t)ti * p.tiles_c);
+                const TileCoord tc = tile_coords(t, p);
+                const int64_t bt = tc.bt;
+                const int32_t ti = tc.ti, tj = tc.tj;
                 const uint32_t fb = ptx::smem_u32(&full_bar[s]);
                 ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
 #pragma unroll
@@ -192,47 +233,58 @@ transpose_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaParams p)
     }
 
     // ------------------------------------ consumers: smem -> registers -> global
-    const int cw = warp - 1;                         // consumer warp id == task id
-    const int box = cw / C::TASKS_PER_BOX;
-    const int tib = cw - box * C::TASKS_PER_BOX;
-    constexpr int CHUNK_GROUPS = 8 / T::CHUNKS_PER_WARP;
-    const int rgrp = tib / CHUNK_GROUPS;             // which ROWS_PER_WARP band of the box
-    const int cgrp = tib - rgrp * CHUNK_GROUPS;      // which chunk group
-    const int b = cgrp * T::CHUNKS_PER_WARP + (lane & ((1 << T::BB) - 1));
-    const int a_lo = (lane >> T::BB) & ((1 << (3 - T::BB)) - 1);
-    const int a_hi = lane >> 3;
-    const int a = rgrp * T::A_PER_WARP + a_hi * (1 << (3 - T::BB)) + a_lo;   // micro-row index
-    const int row_in_box = VEC * a;                  // first of this lane's VEC rows
+    const int cw = warp - 1;
+    // lane -> (a, b) inside one warp-task (see the header comment)
+    const int b_lane = lane & ((1 << T::BB) - 1);
+    const int a_lane = (lane >> 3) * (1 << (3 - T::BB)) + ((lane >> T::BB) & ((1 << (3 - T::BB)) - 1));
+    // warp-task q of this warp: box, first input row of the lane's micro-block, chunk
+    auto task_box = [&](int q) { return (cw + q * CW) / C::TASKS_PER_BOX; };
+    auto task_row = [&](int q) {
+        const int tib = (cw + q * CW) % C::TASKS_PER_BOX;
+        return VEC * ((tib / C::CHUNK_GROUPS) * T::A_PER_WARP + a_lane);
+    };
+    auto task_chunk = [&](int q) {
+        const int tib = (cw + q * CW) % C::TASKS_PER_BOX;
+        return (tib % C::CHUNK_GROUPS) * T::CHUNKS_PER_WARP + b_lane;
+    };
     const int64_t ld_out_b = p.ld_out * ES;
 
     int it = 0;
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-        const int64_t bt = t / tiles_per_mat;
-        const int64_t rem = t - bt * tiles_per_mat;
-        const int32_t ti = (int32_t)(rem / p.tiles_c);
-        const int32_t tj = (int32_t)(rem - (int64_t)ti * p.tiles_c);
+        const TileCoord tc = tile_coords(t, p);
+        const int64_t bt = tc.bt;
+        const int32_t ti = tc.ti, tj = tc.tj;
 
         ptx::mbar_wait(ptx::smem_u32(&full_bar[s]), ph);           // TMA bytes landed
 
-        const uint32_t bbase = smem_base + s * C::STAGE_BYTES + box * C::BOX_BYTES;
-        uint4 r[VEC];
+        const uint32_t sbase = smem_base + s * C::STAGE_BYTES;
+        uint4 r[TPW][VEC];
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-            const int row = row_in_box + k;
-            r[k] = ptx::lds128(bbase + row * 128 + ((b ^ (row & 7)) << 4));
+        for (int q = 0; q < TPW; ++q) {
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                const int row = task_row(q) + k;
+                r[q][k] = ptx::lds128(sbase + task_box(q) * C::BOX_BYTES + row * 128 +
+                                      ((task_chunk(q) ^ (row & 7)) << 4));
+            }
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty_bar[s]));   // release slot
 
-        const int64_t in_row0 = (int64_t)ti * TR + row_in_box;          // = output column
-        const int nvalid = (int)((int64_t)p.rows - in_row0 < VEC ? (int64_t)p.rows - in_row0 : VEC);
-        if (nvalid > 0) {
-            const int64_t orow0 = (int64_t)tj * C::TILE_COLS + box * T::TC + VEC * b;
-            char *out = reinterpret_cast<char *>(p.out) + (bt * p.stride_out + in_row0) * ES;
-            emit_rows<ES>(r, out, ld_out_b, orow0, p.cols, nvalid,
-                          std::make_integer_sequence<int, VEC>{});
+#pragma unroll
+        for (int q = 0; q < TPW; ++q) {
+            const int64_t in_row0 = (int64_t)ti * TR + task_row(q);     // = output column
+            const int64_t left = (int64_t)p.rows - in_row0;
+            const int nvalid = (int)(left < VEC ? left : VEC);
+            if (nvalid > 0) {
+                const int64_t orow0 = (int64_t)tj * C::TILE_COLS + task_box(q) * T::TC +
+                                      VEC * task_chunk(q);
+                char *out = reinterpret_cast<char *>(p.out) + (bt * p.stride_out + in_row0) * ES;
+                emit_rows<ES>(r[q], out, ld_out_b, orow0, p.cols, nvalid,
+                              std::make_integer_sequence<int, VEC>{});
+            }
         }
     }
 }

@@ -51,11 +51,15 @@ def test_sass_is_sm100a_with_tma(lib):
     out = subprocess.run(["cuobjdump", "-sass", desc.lib_path], capture_output=True, text=True,
                          check=True).stdout
     assert "sm_100a" in out
-    tma = [blk for blk in out.split("Function : ")[1:] if "transpose_tma_kernel" in blk[:200]]
-    assert tma, "TMA kernel missing from the cubin"
-    for blk in tma:
-        assert "UTMALDG" in blk, "TMA kernel does not issue cp.async.bulk.tensor"
+    blocks = out.split("Function : ")[1:]
+    tma = [b for b in blocks if "transpose_tma_kernel" in b[:200]]
+    tma2 = [b for b in blocks if "transpose_tma2_kernel" in b[:200]]
+    assert tma and tma2, "TMA kernels missing from the cubin"
+    for blk in tma + tma2:
+        assert "UTMALDG" in blk, "TMA kernel does not issue cp.async.bulk.tensor loads"
         assert "SYNCS" in blk, "TMA kernel does not use mbarriers"
+    for blk in tma2:
+        assert "UTMASTG" in blk, "TMA-store kernel does not issue bulk tensor stores"
 
 
 def test_host_helpers(lib):
@@ -101,12 +105,14 @@ def test_validation_codes(lib):
 
 def test_select_kernel_alignment_rules(lib):
     i, o = FAKE_IN, FAKE_OUT
-    assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "f32") == "tma"
+    assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "f32") == "tma_st"
+    assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "u8") == "tma"
+    assert desc.desc_select_kernel(i, o, 1, 2, 64, 64, 4, 0, 0, "f32") == "tma"
     assert desc.desc_select_kernel(i + 4, o, 1, 64, 64, 64, 64, 0, 0, "f32") == "smem"
     assert desc.desc_select_kernel(i, o, 1, 3000, 5001, 5001, 3000, 0, 0, "f64") == "smem"
-    assert desc.desc_select_kernel(i, o, 1, 3000, 5000, 5000, 3000, 0, 0, "f64") == "tma"
+    assert desc.desc_select_kernel(i, o, 1, 3000, 5000, 5000, 3000, 0, 0, "f64") == "tma_st"
     assert desc.desc_select_kernel(i, o, 1, 3, 5, 5, 3, 0, 0, "f32") == "smem"
-    assert desc.desc_select_kernel(i, o, 2, 64, 64, 64, 64, 4096, 4096, "f32") == "tma"
+    assert desc.desc_select_kernel(i, o, 2, 64, 64, 64, 64, 4096, 4096, "f32") == "tma_st"
     assert desc.desc_select_kernel(i, o, 2, 64, 64, 64, 64, 4097, 4096, "f32") == "smem"
 
 

@@ -79,22 +79,24 @@ def run_case(batch, rows, cols, es, kernel="auto", ld_in=None, ld_out=None, stri
     body = host[GUARD + out_off:GUARD + out_off + out_bytes].view(ut)
     # expected: oracle into a sentinel-filled buffer of the same layout
     exp = np.frombuffer(bytes([SENT]) * out_bytes, dtype=ut).copy()
-    if n_out:
-        oracle.transpose_raw(np.ascontiguousarray(src), exp, batch, rows, cols, cols, ld_out,
-                             rows * cols, stride_out, es)
+    if n_out:   # the oracle reads the very same raw input buffer (overlapping inputs too)
+        oracle.transpose_raw(inbuf, exp, batch, rows, cols, ld_in, ld_out, stride_in,
+                             stride_out, es)
     if body.tobytes() != exp.tobytes():
         bad = np.nonzero(body != exp)[0]
         raise AssertionError(f"{bad.size} mismatching elements, first at flat {bad[:8]}")
     return sel
 
 
-KERNELS = ["auto", "smem", "tma"]
+KERNELS = ["auto", "smem", "tma", "tma_st"]
 
 
 def _kernels_for(es, rows, cols, ld_in, ld_out):
     ks = ["auto", "smem"]
     if (ld_in * es) % 16 == 0 and (ld_out * es) % 16 == 0:
         ks.append("tma")
+        if es in (4, 8) and rows * es >= 16:
+            ks.append("tma_st")
     return ks
 
 
@@ -134,7 +136,7 @@ def test_tight_ld_odd_shapes_fall_back(es):
 @pytest.mark.parametrize("es", [4, 8])
 def test_padded_ld_guard_bands(es):
     """T4: 67x131 with ld_in=136, ld_out=72: padding columns and guard bands untouched."""
-    for k in ("auto", "tma", "smem"):
+    for k in ("auto", "tma", "tma_st", "smem"):
         run_case(1, 67, 131, es, k, ld_in=136, ld_out=72)
 
 
@@ -143,15 +145,16 @@ def test_misaligned_base(es):
     """Base offsets that break 16-byte alignment route to the SMEM kernel and stay exact."""
     assert run_case(1, 100, 200, es, in_off=es) == "smem"
     assert run_case(1, 100, 200, es, out_off=es) == "smem"
-    with pytest.raises(desc.DescError, match="DESC_ERR_KERNEL"):
-        run_case(1, 100, 200, es, "tma", in_off=es, check=False)
+    for k in ("tma", "tma_st"):
+        with pytest.raises(desc.DescError, match="DESC_ERR_KERNEL"):
+            run_case(1, 100, 200, es, k, in_off=es, check=False)
 
 
 @pytest.mark.parametrize("es", [4, 8])
 def test_batched_odd_strides(es):
     """T7: 7 x (33 x 65) with strides that leave gaps; input strides overlapping allowed."""
     v = 16 // es
-    for k in ("auto", "smem", "tma"):
+    for k in ("auto", "smem", "tma", "tma_st"):
         run_case(7, 33, 65, es, k, ld_in=65 + (-65) % v, ld_out=40, stride_in=33 * 72 + v,
                  stride_out=65 * 40 + 2 * v)
     run_case(5, 20, 24, es, "smem", ld_in=24, ld_out=20, stride_in=24 * 10, stride_out=480)
@@ -211,7 +214,7 @@ def test_config2_8192_f32_and_i32():
     a = synth.random_bits((1, 8192, 8192), 4, synth.BASE_SEED + 2)
     x = torch.from_numpy(a[0].view(np.int32)).cuda()
     ref = oracle.transpose(a[0])
-    for k in ("auto", "tma", "smem"):
+    for k in ("auto", "tma", "tma_st", "smem"):
         for dt in (torch.float32, torch.int32):
             y = desc.transpose(x.view(dt), kernel=k)
             torch.cuda.synchronize()
@@ -220,7 +223,7 @@ def test_config2_8192_f32_and_i32():
 
 def test_config3_3000x5000_f64_and_misaligned_ld():
     a = synth.random_bits((1, 3000, 5000), 8, synth.BASE_SEED + 3)
-    assert run_case(1, 3000, 5000, 8, src=a) == "tma"
+    assert run_case(1, 3000, 5000, 8, src=a) == "tma_st"
     assert run_case(1, 3000, 5000, 8, ld_in=5001, src=a) == "smem"
 
 
