@@ -127,8 +127,26 @@ desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
                                int64_t ld_out, int64_t stride_in,
                                int64_t stride_out, desc_dtype dtype);
 
-/* Number of kernel launches the last successful device call of this thread
- * issued (0 for an empty shape, 1 otherwise). */
+/* Host-buffer transpose (same operation and layout rules as desc_transpose_batched,
+ * but h_in / h_out are HOST memory -- pinned for full PCIe overlap, pageable works).
+ * The library streams row bands of the input through the caller-provided device
+ * workspace d_work (256-byte aligned, work_bytes >= desc_transpose_host_workspace
+ * recommended; smaller works down to one row): H2D copy of band k+1, transpose of
+ * band k and D2H copy of band k-1 overlap on two internal streams.  Asynchronous on
+ * `stream` like the device entry points: the host buffers must stay valid and
+ * untouched until the stream reaches the end of the operation.  h_in/h_out that are
+ * device memory give DESC_ERR_MEMSPACE; a too-small workspace gives DESC_ERR_SHAPE. */
+desc_status desc_transpose_host(const void *h_in, void *h_out, int64_t batch,
+                                int64_t rows, int64_t cols, int64_t ld_in,
+                                int64_t ld_out, int64_t stride_in,
+                                int64_t stride_out, desc_dtype dtype, void *d_work,
+                                size_t work_bytes, void *stream);
+
+/* Recommended workspace bytes for desc_transpose_host (double-buffered 1024-row bands). */
+size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);
+
+/* Number of kernel launches the last successful call of this thread issued (0 for an
+ * empty shape, 1 per device call, one per band for desc_transpose_host). */
 int desc_last_launch_count(void);
 
 const char *desc_status_string(desc_status s);

@@ -20,7 +20,8 @@ __all__ = [
     "DescError", "DTYPE", "KERNEL", "lib_path", "load",
     "desc_transpose", "desc_transpose_batched", "desc_transpose_ex", "desc_select_kernel",
     "desc_status_string", "desc_last_error", "desc_dtype_size", "desc_version",
-    "desc_last_launch_count", "transpose", "transpose_batched",
+    "desc_last_launch_count", "desc_transpose_host", "desc_transpose_host_workspace",
+    "transpose", "transpose_batched", "transpose_host",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -62,6 +63,11 @@ def load():
     lib.desc_transpose_ex.restype = ci
     lib.desc_select_kernel.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci]
     lib.desc_select_kernel.restype = ci
+    lib.desc_transpose_host.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci, vp,
+                                        ctypes.c_size_t, vp]
+    lib.desc_transpose_host.restype = ci
+    lib.desc_transpose_host_workspace.argtypes = [i64, i64, ci]
+    lib.desc_transpose_host_workspace.restype = ctypes.c_size_t
     lib.desc_last_launch_count.argtypes = []
     lib.desc_last_launch_count.restype = ci
     lib.desc_status_string.argtypes = [ci]
@@ -107,6 +113,17 @@ def desc_select_kernel(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride
     k = load().desc_select_kernel(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out,
                                   stride_in, stride_out, _dt(dtype))
     return KERNEL_NAME[k]
+
+
+def desc_transpose_host(h_in_ptr, h_out_ptr, batch, rows, cols, ld_in, ld_out, stride_in,
+                        stride_out, dtype, d_work_ptr, work_bytes, stream=0):
+    return _check(load().desc_transpose_host(h_in_ptr, h_out_ptr, batch, rows, cols, ld_in,
+                                             ld_out, stride_in, stride_out, _dt(dtype),
+                                             d_work_ptr, work_bytes, stream))
+
+
+def desc_transpose_host_workspace(rows, cols, dtype) -> int:
+    return load().desc_transpose_host_workspace(rows, cols, _dt(dtype))
 
 
 def desc_status_string(status: int) -> str:
@@ -196,4 +213,32 @@ def transpose_batched(x, out=None, kernel: str = "auto"):
     stride_out = out.stride(0) if batch > 1 else 0
     desc_transpose_ex(x.data_ptr(), out.data_ptr(), batch, rows, cols, ld_in, ld_out,
                       stride_in, stride_out, x.dtype, kernel, _stream_of(x))
+    return out
+
+
+def transpose_host(x, out=None, work=None):
+    """out = x^T (or per-matrix for 3-D) for CPU tensors (pin them for PCIe overlap),
+    streamed through the GPU by desc_transpose_host on the current CUDA stream.
+    `work` is an optional uint8 CUDA tensor used as the device workspace."""
+    import torch
+    if x.device.type != "cpu":
+        raise ValueError("transpose_host takes host (CPU) tensors")
+    x3 = x if x.dim() == 3 else x.unsqueeze(0)
+    batch, rows, cols = x3.shape
+    if out is None:
+        out = torch.empty((batch, cols, rows) if x.dim() == 3 else (cols, rows), dtype=x.dtype,
+                          pin_memory=x.is_pinned())
+    o3 = out if out.dim() == 3 else out.unsqueeze(0)
+    if tuple(o3.shape) != (batch, cols, rows) or out.dtype != x.dtype:
+        raise ValueError("out has the wrong shape or dtype")
+    if work is None:
+        nbytes = desc_transpose_host_workspace(rows, cols, x.dtype)
+        work = torch.empty(max(nbytes, 256), dtype=torch.uint8, device="cuda")
+    ld_in = x3.stride(1) if rows > 1 else cols
+    ld_out = o3.stride(1) if cols > 1 else rows
+    stride_in = x3.stride(0) if batch > 1 else 0
+    stride_out = o3.stride(0) if batch > 1 else 0
+    desc_transpose_host(x3.data_ptr(), o3.data_ptr(), batch, rows, cols, ld_in, ld_out,
+                        stride_in, stride_out, x.dtype, work.data_ptr(), work.numel(),
+                        torch.cuda.current_stream(work.device).cuda_stream)
     return out

@@ -222,6 +222,26 @@ int tile_group(int grid, int tr, int tc, int tiles_r) {
 bool tma_store_ok(const Args &a) { return (a.es == 4 || a.es == 8) && a.rows * a.es >= 16; }
 
 // ---- launchers -----------------------------------------------------------------------
+// Launch with programmatic stream serialisation (PDL) so that back-to-back transposes
+// overlap launch latency and prologue with the previous kernel's tail; the kernels call
+// griddepcontrol.wait before touching global memory, so stream order is preserved.
+template <typename Kern, typename... Args_>
+cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
+                       Args_... args) {
+    static const int pdl = dev_knob("DESC_PDL", 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Shared launch plumbing of the persistent TMA kernels: dynamic-smem opt-in (once per
 // kernel instantiation), grid = min(tiles, SMs x occupancy), tile raster parameters.
 template <typename Kern>
@@ -270,8 +290,9 @@ desc_status launch_tma(const Args &a) {
         return s;
     CUtensorMap map;
     if (desc_status s = in_map(a, TR, &map)) return s;
-    kern<<<grid, C::THREADS, C::SMEM_BYTES, a.stream>>>(map, p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(kern, grid, C::THREADS, C::SMEM_BYTES, a.stream, map, p);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose_tma_kernel launch");
+    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "transpose_tma_kernel launch");
     g_last_launches = 1;
     return DESC_OK;
@@ -288,8 +309,9 @@ desc_status launch_tma2(const Args &a) {
     CUtensorMap min, mout;
     if (desc_status s = in_map(a, TR, &min)) return s;
     if (desc_status s = out_map(a, C::TILE_COLS, &mout)) return s;
-    kern<<<grid, C::THREADS, C::SMEM_BYTES, a.stream>>>(min, mout, p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(kern, grid, C::THREADS, C::SMEM_BYTES, a.stream, min, mout, p);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose_tma2_kernel launch");
+    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "transpose_tma2_kernel launch");
     g_last_launches = 1;
     return DESC_OK;
@@ -359,7 +381,11 @@ desc_status run_tma(const Args &a) {
 }
 
 desc_status run_tma2(const Args &a) {
-    const int cfg = tma_cfg();
+    int cfg = tma_cfg();
+    // Small problems (< 64 MB per call): smaller tiles for more CTAs per SM and a
+    // finer tail (gpurun_out/sweep_small_tma_st.txt: 2048^2 f64 16.4 -> 14.4 us).
+    const bool small = a.batch * a.rows * a.cols * a.es < ((int64_t)64 << 20);
+    if (cfg == 0 && small) cfg = 11;
     switch (a.es) {
         case 4:
             switch (cfg) {
@@ -373,7 +399,8 @@ desc_status run_tma2(const Args &a) {
                 case 8: return launch_tma2<4, 256, 1, 4, 8, 2>(a);
                 case 9: return launch_tma2<4, 128, 2, 2, 8, 2>(a);
                 case 10: return launch_tma2<4, 256, 1, 2, 4, 2>(a);
-                case 11: return launch_tma2<4, 128, 1, 2, 8, 2>(a);
+                case 11: return launch_tma2<4, 64, 2, 2, 8, 2>(a);
+                case 13: return launch_tma2<4, 128, 1, 2, 8, 2>(a);
                 case 12: return launch_tma2<4, 128, 1, 4, 8, 2>(a);
                 // tuned (gpurun_out sweeps, profiles/): 128 x 64 tile, 2-stage ring,
                 // 2 output buffers, 8 consumer warps, 1 CTA (288 threads, 129 KB) per SM
@@ -465,11 +492,7 @@ desc_status validate(const Args &a, bool *empty) {
     return DESC_OK;
 }
 
-desc_status run(const Args &a, desc_kernel k) {
-    g_last_launches = 0;
-    bool empty;
-    if (desc_status s = validate(a, &empty)) return s;
-    if (empty) return DESC_OK;
+desc_status dispatch(const Args &a, desc_kernel k) {
     const bool tma_ok = tma_eligible(a);
     if (k == DESC_KERNEL_TMA && !tma_ok)
         return fail(DESC_ERR_KERNEL, "TMA kernel needs 16-byte aligned bases, ld*size and stride*size");
@@ -482,6 +505,150 @@ desc_status run(const Args &a, desc_kernel k) {
     if (k == DESC_KERNEL_AUTO && tma_store_ok(a)) return run_tma2(a);
     if (k == DESC_KERNEL_TMA || k == DESC_KERNEL_AUTO) return run_tma(a);
     return fail(DESC_ERR_KERNEL, "unknown kernel variant %d", (int)k);
+}
+
+desc_status run(const Args &a, desc_kernel k) {
+    g_last_launches = 0;
+    bool empty;
+    if (desc_status s = validate(a, &empty)) return s;
+    if (empty) return DESC_OK;
+    return dispatch(a, k);
+}
+
+// ---- host-buffer pipeline (desc_transpose_host) ---------------------------------------
+// Two internal streams per device alternate over row bands of the input so that the H2D
+// copy of band k+1, the transpose of band k and the D2H copy of band k-1 overlap (PCIe is
+// full duplex).  The caller's stream is joined at entry and exit with events, so the call
+// stays asynchronous and ordered on `stream`.
+struct HostPipe {
+    bool init = false;
+    cudaStream_t s[2];
+    cudaEvent_t enter, done[2];
+};
+std::mutex g_pipe_mu;
+HostPipe g_pipe[64];
+
+desc_status host_pipe(int dev, HostPipe **out) {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    HostPipe &hp = g_pipe[dev];
+    if (!hp.init) {
+        cudaError_t e;
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_fail(e, "cudaStreamCreateWithFlags");
+            if ((e = cudaEventCreateWithFlags(&hp.done[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cudaEventCreateWithFlags");
+        }
+        if ((e = cudaEventCreateWithFlags(&hp.enter, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "cudaEventCreateWithFlags");
+        hp.init = true;
+    }
+    *out = &hp;
+    return DESC_OK;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Device bytes one band of `band_rows` input rows needs (input band + output band, both
+// with 16-byte padded pitches so the TMA kernels apply), double-buffered.
+int64_t band_bytes(int64_t band_rows, int64_t cols, int es) {
+    const int64_t v = 16 / es;
+    const int64_t in_b = round_up(band_rows * round_up(cols, v) * es, 256);
+    const int64_t out_b = round_up(cols * round_up(band_rows, v) * es, 256);
+    return 2 * (in_b + out_b);
+}
+
+desc_status check_host_ptr(const void *p, const char *name) {
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return DESC_OK;   // unknown to CUDA: plain pageable host memory
+    }
+    if (attr.type == cudaMemoryTypeDevice)
+        return fail(DESC_ERR_MEMSPACE, "%s is device memory; desc_transpose_host takes host buffers", name);
+    return DESC_OK;
+}
+
+desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows, int64_t cols,
+                     int64_t ld_in, int64_t ld_out, int64_t stride_in, int64_t stride_out, int es,
+                     void *d_work, size_t work_bytes, cudaStream_t stream) {
+    g_last_launches = 0;
+    if (es == 0) return fail(DESC_ERR_DTYPE, "unknown dtype");
+    if (batch < 0 || rows < 0 || cols < 0) return fail(DESC_ERR_SHAPE, "negative size");
+    if (batch == 0 || rows == 0 || cols == 0) return DESC_OK;
+    if (!h_in || !h_out || !d_work) return fail(DESC_ERR_NULL, "null pointer");
+    if (ld_in < cols || ld_out < rows) return fail(DESC_ERR_SHAPE, "ld smaller than the row extent");
+    if (stride_in < 0 || stride_out < 0) return fail(DESC_ERR_SHAPE, "negative batch stride");
+    if (batch > 1 && stride_out < (cols - 1) * ld_out + rows)
+        return fail(DESC_ERR_SHAPE, "batched outputs overlap");
+    int64_t span_in, span_out, bin, bout;
+    if (!span_elems(batch, rows, cols, ld_in, stride_in, &span_in) ||
+        !span_elems(batch, cols, rows, ld_out, stride_out, &span_out) ||
+        !mul_ok(span_in, es, &bin) || !mul_ok(span_out, es, &bout))
+        return fail(DESC_ERR_SHAPE, "extent overflows int64");
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(h_in), o0 = reinterpret_cast<uintptr_t>(h_out);
+    if (i0 < o0 + (uintptr_t)bout && o0 < i0 + (uintptr_t)bin)
+        return fail(DESC_ERR_ALIAS, "host in and out overlap (&uniq, P:576-579)");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (desc_status s = check_host_ptr(h_in, "h_in")) return s;
+    if (desc_status s = check_host_ptr(h_out, "h_out")) return s;
+    if (desc_status s = check_memspace(d_work, dev, "d_work")) return s;
+    if ((reinterpret_cast<uintptr_t>(d_work) & 255) != 0)
+        return fail(DESC_ERR_SHAPE, "d_work must be 256-byte aligned");
+
+    // largest band (multiple of 128 rows when possible) whose double buffers fit d_work
+    int64_t band = rows;
+    while (band > 1 && band_bytes(band, cols, es) > (int64_t)work_bytes)
+        band = band > 256 ? (band / 2 + 127) / 128 * 128 : band / 2;
+    if (band_bytes(band, cols, es) > (int64_t)work_bytes)
+        return fail(DESC_ERR_SHAPE, "d_work (%zu bytes) too small: need >= %lld", work_bytes,
+                    (long long)band_bytes(1, cols, es));
+
+    HostPipe *hp;
+    if (desc_status s = host_pipe(dev, &hp)) return s;
+    const int64_t v = 16 / es;
+    const int64_t ldi_d = round_up(cols, v);
+    const int64_t in_b = round_up(band * ldi_d * es, 256);
+    const int64_t out_b = round_up(cols * round_up(band, v) * es, 256);
+    char *w = static_cast<char *>(d_work);
+    char *d_in[2] = {w, w + in_b};
+    char *d_out[2] = {w + 2 * in_b, w + 2 * in_b + out_b};
+
+    if ((e = cudaEventRecord(hp->enter, stream)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    for (int i = 0; i < 2; ++i)
+        if ((e = cudaStreamWaitEvent(hp->s[i], hp->enter, 0)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamWaitEvent");
+    int launches = 0;
+    int64_t k = 0;
+    for (int64_t b = 0; b < batch; ++b) {
+        for (int64_t r0 = 0; r0 < rows; r0 += band, ++k) {
+            const int64_t nr = rows - r0 < band ? rows - r0 : band;
+            const int buf = (int)(k & 1);
+            cudaStream_t s = hp->s[buf];
+            const int64_t ldo_d = round_up(nr, v);
+            const char *src = static_cast<const char *>(h_in) + (b * stride_in + r0 * ld_in) * es;
+            e = cudaMemcpy2DAsync(d_in[buf], ldi_d * es, src, ld_in * es, cols * es, nr,
+                                  cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync H2D");
+            Args a{d_in[buf], d_out[buf], 1, nr, cols, ldi_d, ldo_d, 0, 0, es, s};
+            if (desc_status st = dispatch(a, DESC_KERNEL_AUTO)) return st;
+            ++launches;
+            char *dst = static_cast<char *>(h_out) + (b * stride_out + r0) * es;
+            e = cudaMemcpy2DAsync(dst, ld_out * es, d_out[buf], ldo_d * es, nr * es, cols,
+                                  cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync D2H");
+        }
+    }
+    for (int i = 0; i < 2; ++i) {
+        if ((e = cudaEventRecord(hp->done[i], hp->s[i])) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+        if ((e = cudaStreamWaitEvent(stream, hp->done[i], 0)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamWaitEvent");
+    }
+    g_last_launches = launches;
+    return DESC_OK;
 }
 
 }  // namespace
@@ -516,6 +683,21 @@ desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch, i
            dtype_size(dtype), nullptr};
     if (a.es == 0 || !tma_eligible(a)) return DESC_KERNEL_SMEM;
     return tma_store_ok(a) ? DESC_KERNEL_TMA_ST : DESC_KERNEL_TMA;
+}
+
+desc_status desc_transpose_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
+                                int64_t cols, int64_t ld_in, int64_t ld_out, int64_t stride_in,
+                                int64_t stride_out, desc_dtype dtype, void *d_work,
+                                size_t work_bytes, void *stream) {
+    return run_host(h_in, h_out, batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
+                    dtype_size(dtype), d_work, work_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype) {
+    const int es = dtype_size(dtype);
+    if (es == 0 || rows <= 0 || cols <= 0) return 0;
+    const int64_t band = rows < 1024 ? rows : 1024;
+    return (size_t)band_bytes(band, cols, es);
 }
 
 int desc_last_launch_count(void) { return g_last_launches; }

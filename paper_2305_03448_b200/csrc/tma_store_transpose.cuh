@@ -118,6 +118,10 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
         ptx::fence_mbarrier_init();
     }
     __syncthreads();
+    // PDL: the prologue above may overlap the previous kernel's tail; nothing below touches
+    // global memory before every prerequisite grid has completed.
+    ptx::grid_dependency_wait();
+    ptx::grid_launch_dependents();
 
     if (warp == 0) {
         // ------------------------------ producer: one elected lane issues TMA loads

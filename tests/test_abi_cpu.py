@@ -103,6 +103,23 @@ def test_validation_codes(lib):
     assert _status("desc_transpose_ex", i, o, 1, 4, 4, 4, 4, 0, 0, 0, 2, None) in (5, 6)
 
 
+def test_host_entry_validation(lib):
+    import numpy as np
+    h_in = np.zeros(64, dtype=np.float32)
+    h_out = np.zeros(64, dtype=np.float32)
+    f = "desc_transpose_host"
+    args = (h_in.ctypes.data, h_out.ctypes.data)
+    assert _status(f, *args, 1, 0, 8, 8, 8, 0, 0, 0, FAKE_OUT, 4096, None) == 0     # empty
+    assert _status(f, None, h_out.ctypes.data, 1, 8, 8, 8, 8, 0, 0, 0, FAKE_OUT, 4096, None) == 1
+    assert _status(f, *args, 1, 8, 8, 8, 8, 0, 0, 0, None, 4096, None) == 1         # no workspace
+    assert _status(f, *args, 1, 8, 8, 7, 8, 0, 0, 0, FAKE_OUT, 4096, None) == 2     # ld_in < cols
+    assert _status(f, *args, 1, 8, 8, 8, 8, 0, 0, 42, FAKE_OUT, 4096, None) == 3    # dtype
+    assert _status(f, h_in.ctypes.data, h_in.ctypes.data, 1, 8, 8, 8, 8, 0, 0, 0, FAKE_OUT,
+                   4096, None) == 4                                                # alias
+    assert desc.desc_transpose_host_workspace(8192, 8192, "f32") == 2 * 2 * 1024 * 8192 * 4
+    assert desc.desc_transpose_host_workspace(0, 8, "f32") == 0
+
+
 def test_select_kernel_alignment_rules(lib):
     i, o = FAKE_IN, FAKE_OUT
     assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "f32") == "tma_st"

@@ -257,3 +257,35 @@ def test_config5_65536_f32_sampled():
         assert got.tobytes() == exp.tobytes(), (i0, j0)
     del x, y
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------ host-buffer entry point
+@pytest.mark.parametrize("pinned", [True, False])
+def test_transpose_host_bands(pinned):
+    """desc_transpose_host: pinned and pageable host buffers, a workspace small enough to
+    force many row bands, ragged shapes, f32 and f64, plus a batched case."""
+    for (batch, rows, cols, es) in ((1, 1000, 777, 4), (1, 333, 1024, 8), (3, 130, 257, 4)):
+        src = synth.random_bits((batch, rows, cols), es, rows + cols)
+        x = torch.from_numpy(src.view(NP_INT[es]))
+        if pinned:
+            x = x.pin_memory()
+        for work_rows in (64, 100000):
+            nbytes = desc.desc_transpose_host_workspace(min(rows, work_rows), cols, DT_OF_ES[es])
+            work = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+            y = desc.transpose_host(x if batch > 1 else x[0], work=work)
+            torch.cuda.synchronize()
+            assert desc.desc_last_launch_count() >= 1
+            got = y.numpy().view(synth.UINT_OF_SIZE[es])
+            assert got.tobytes() == oracle.transpose(src if batch > 1 else src[0]).tobytes()
+
+
+def test_transpose_host_rejects_device_buffers():
+    d = torch.empty((64, 64), dtype=torch.float32, device="cuda")
+    work = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    h = torch.empty((64, 64), dtype=torch.float32)
+    with pytest.raises(desc.DescError, match="DESC_ERR_MEMSPACE"):
+        desc.desc_transpose_host(d.data_ptr(), h.data_ptr(), 1, 64, 64, 64, 64, 0, 0, "f32",
+                                 work.data_ptr(), work.numel())
+    with pytest.raises(desc.DescError, match="DESC_ERR_SHAPE"):
+        desc.desc_transpose_host(h.data_ptr(), torch.empty_like(h).data_ptr(), 1, 64, 64, 64, 64,
+                                 0, 0, "f32", work.data_ptr(), 16)
