@@ -48,7 +48,10 @@ WORKLOADS = {
                          name="3000x5000 f64 non-tile-multiple transpose (BASELINE.json configs[2])"),
     "batched": dict(batch=256, rows=1024, cols=1024, dtype="f32", es=4, shard=True,
                     name="batched 256x(1024x1024) f32, batch sharded over ranks (BASELINE.json configs[3])"),
+    "dist65536": dict(batch=1, rows=65536, cols=65536, dtype="f32", es=4, dist=True,
+                      name="65536x65536 f32 distributed transpose, row slabs + exchange (BASELINE.json configs[4])"),
 }
+NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU
 
 
 def load_peak():
@@ -168,6 +171,8 @@ def run_oracle(wl, budget_s: float, steps: int | None = None, warmup: int = 0,
     import oracle
     es, rows, cols, batch = wl["es"], wl["rows"], wl["cols"], wl["batch"]
     sample_batch = min(batch, 4)
+    if wl.get("dist"):     # bounded sample of the 16 GiB matrix: a 4096-row slab of it
+        rows, wl = 4096, dict(wl, name=wl["name"] + " (4096-row slab sample)")
     a = synth.random_bits((sample_batch, rows, cols), es, synth.BASE_SEED + 2)
     out = np.empty((sample_batch, cols, rows), dtype=a.dtype)
 
@@ -299,8 +304,13 @@ def ours_arm(args, wl, world, rank, local):
         step()
     torch.cuda.synchronize(dev)
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # Timed region.  Without an L2 flush the K launches run back to back and only the two
+    # region events are recorded (events between launches would add ~5 us gaps and block
+    # the PDL overlap); the kernel's average launch duration is then region / launches
+    # (nothing else runs on the stream).  With a flush, each launch is bracketed by its own
+    # events and only the launches are summed.
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if flush else []
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if flush else []
     region0 = torch.cuda.Event(enable_timing=True)
     region1 = torch.cuda.Event(enable_timing=True)
     launches = 0
@@ -312,27 +322,38 @@ def ours_arm(args, wl, world, rank, local):
         for k in range(args.steps):
             if flush:
                 l2_flush()             # evict the working set from the 126 MB L2 (clean)
-            starts[k].record(stream)
+                starts[k].record(stream)
             launches += step()
-            ends[k].record(stream)
+            if flush:
+                ends[k].record(stream)
         region1.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    per_launch = [s.elapsed_time(e) for s, e in zip(starts, ends)]   # ms, device time
     region_ms = region0.elapsed_time(region1)
-    kern_ms_sum = sum(per_launch)
-    # timed quantity: the region (== sum of launches when there is no flush)
-    timed_ms = kern_ms_sum if flush else region_ms
-    t = torch.tensor([timed_ms, kern_ms_sum], dtype=torch.float64, device=dev)
+    if flush:
+        per_launch = [s.elapsed_time(e) for s, e in zip(starts, ends)]   # ms, device time
+        timed_ms = sum(per_launch)
+    else:
+        timed_ms = region_ms
+    t = torch.tensor([timed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    timed_ms_max, kern_ms_max = t.tolist()
+    timed_ms_max = t.item()
 
     total_bytes = step_bytes * world * args.steps
     value = total_bytes / (timed_ms_max / 1e3) / 1e9
-    avg_launch_ms = statistics.mean(per_launch)
+    avg_launch_ms = timed_ms / launches            # this rank's average launch duration
     achieved = step_bytes / (avg_launch_ms / 1e3) / 1e9
+    if not flush:  # untimed diagnostic pass: per-launch spread (events between launches)
+        n_diag = min(args.steps, 200)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_diag)]
+        for k in range(n_diag):
+            ev[2 * k].record(stream)
+            step()
+            ev[2 * k + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        per_launch = [ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(n_diag)]
     peak, peak_src = load_peak()
 
     # ---- parity of the timed output (rank-local) ------------------------------------
@@ -369,13 +390,17 @@ def ours_arm(args, wl, world, rank, local):
                        "parallelism": f"{world} independent replica(s), no collective",
                        "l2": ("flushed before every step (read of a 252 MiB buffer, untimed)" if flush else
                               f"inputs larger than L2 ({batch * mat_bytes / 1e6:.0f} MB > 126 MB), no flush"),
-                       "timing": "CUDA events on the launch stream, max over ranks"},
+                       "timing": ("CUDA events on the launch stream around the K launches "
+                                  "(per launch when flushing), max over ranks")},
             "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(args.workload), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes,
                          "kernel": KERNEL_FN[selected],
+                         "launch_ms_mean_in_region": round(avg_launch_ms, 5),
+                         "launch_spread_from": ("the timed launches" if flush else
+                                                "an untimed pass with events around each launch"),
                          "launch_ms_median": round(statistics.median(per_launch), 5),
                          "launch_ms_p10": round(float(np.percentile(per_launch, 10)), 5),
                          "launch_ms_p90": round(float(np.percentile(per_launch, 90)), 5),
@@ -387,6 +412,115 @@ def ours_arm(args, wl, world, rank, local):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def dist_arm(args, wl, world, rank, local):
+    """configs[4]: the global M x N matrix lives as row slabs, one per rank; a step is one
+    full distributed transpose (slab_transpose over NCCL, or the fused IPC peer path)."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    import paper_2305_03448_b200 as desc
+    from paper_2305_03448_b200 import dist as ddist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    desc.load()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    M = N = args.dist_n
+    es = wl["es"]
+    lay = ddist.SlabLayout(M, N, world, rank)
+    seed = synth.BASE_SEED + 5
+    x = torch.empty((lay.Rm, N), dtype=torch.int32, device=dev)
+    synth.hash_fill_torch(x, lay.in_rows()[0], 0, N, seed, chunk_rows=1024)
+    x = x.view(torch.float32)
+    out = torch.empty((lay.Rn, M), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    impl = args.dist_impl if world > 1 else "local"
+    if impl == "p2p":
+        xp = ddist.PeerSlabTranspose(out, M)
+        step = lambda: xp(x)[1]                                      # noqa: E731
+    else:
+        ws = None
+        if world > 1:
+            ws = (torch.empty(lay.Rm * N, dtype=torch.float32, device=dev),
+                  torch.empty(lay.Rm * N, dtype=torch.float32, device=dev))
+
+        def step():
+            ddist.slab_transpose(x, out, workspace=ws)
+            return 2 if world > 1 else 1                             # our kernels per step
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            launches += step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    step_s = ms_max / args.steps / 1e3
+    total = 2 * M * N * es
+    value = total * args.steps / (ms_max / 1e3) / 1e9
+    peak, peak_src = load_peak()
+    S = lay.Rm * N * es
+    t_hbm = 2 * S / (peak * 1e9)
+    t_nvl = lay.nvlink_bytes(es) / (NVLINK_PEER_GBS * 1e9)
+    t_star = max(t_hbm, t_nvl)
+    # sampled parity: 64 x 64 blocks of this rank's output slab vs the oracle
+    rng = np.random.default_rng(seed + rank)
+    r0, _ = lay.out_rows()
+    picks = [(0, 0), (lay.Rn - 64, M - 64)] + [
+        (int(rng.integers(0, lay.Rn - 64)), int(rng.integers(0, M - 64))) for _ in range(6)]
+    ok = True
+    for j0, i0 in picks:           # out_r[j0:j0+64, i0:i0+64] = A[i0:i0+64, r0+j0:r0+j0+64]^T
+        ii, jj = np.meshgrid(np.arange(i0, i0 + 64), np.arange(r0 + j0, r0 + j0 + 64), indexing="ij")
+        exp = oracle.transpose(synth.hash_expected_np(ii, jj, N, seed, es))
+        got = out[j0:j0 + 64, i0:i0 + 64].view(torch.int32).cpu().numpy().view(np.uint32)
+        ok &= got.tobytes() == exp.tobytes()
+    okt = torch.tensor([1 if ok else 0], device=dev)
+    if world > 1:
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"],
+            "data": "synthetic (counter-based hash, generated in HBM)",
+            "config": {"workload": wl["name"], "rows": M, "cols": N, "ranks": world,
+                       "slab_rows": lay.Rm, "impl": impl,
+                       "parallelism": f"row slabs over {world} rank(s)",
+                       "l2": "inputs larger than L2, no flush",
+                       "timing": "CUDA events around K steps, max over ranks"},
+            "roofline": {"bound": "hbm" if t_hbm >= t_nvl else "nvlink",
+                         "achieved": round((2 * S if t_hbm >= t_nvl else lay.nvlink_bytes(es))
+                                           / step_s / 1e9, 2),
+                         "peak": peak if t_hbm >= t_nvl else NVLINK_PEER_GBS,
+                         "unit": "GB/s", "frac": round(t_star / step_s, 4), "traffic": None,
+                         "t_star_ms": round(t_star * 1e3, 4), "t_hbm_ms": round(t_hbm * 1e3, 4),
+                         "t_nvlink_ms": round(t_nvl * 1e3, 4), "peak_source": peak_src,
+                         "note": "frac = T*/t_step, T* = max(2S/HBM, S(P-1)/P / 770 GB/s)"},
+            "parity": "sampled 64x64 blocks bit-exact vs oracle" if okt.item() else "MISMATCH",
+            "gpu_launches": launches, "cpu_baseline": None, "e2e": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if impl == "p2p":
+        xp.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -447,6 +581,8 @@ def main():
     ap.add_argument("--reference-seconds", type=float, default=120.0)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--dist-impl", choices=["nccl", "p2p"], default="nccl")
+    ap.add_argument("--dist-n", type=int, default=65536)
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -456,6 +592,8 @@ def main():
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
     wl = dict(WORKLOADS[args.workload])
+    if wl.get("dist") and args.impl == "ours":
+        return dist_arm(args, wl, world, rank, local)
     if args.impl == "reference":
         return reference_arm(args, wl, world, rank)
     return ours_arm(args, wl, world, rank, local)

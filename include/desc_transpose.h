@@ -24,16 +24,18 @@
  *   `in` is a shared, read-only borrow; `out` is a unique borrow until the
  *   stream reaches the operation.  The byte ranges spanned by in and out must
  *   not overlap (DESC_ERR_ALIAS); in-place transposition is not supported.
- *   For batch > 1 the output matrices must be pairwise disjoint:
- *   stride_out >= (cols-1)*ld_out + rows (the narrowing rule), else
- *   DESC_ERR_SHAPE.  Input matrices may overlap (read-only).  Strides must be >= 0.
+ *   For batch > 1 the output matrices must be pairwise disjoint (the narrowing
+ *   rule), in one of two layouts: stacked, stride_out >= (cols-1)*ld_out
+ *   + rows; or side by side within each output row, stride_out >= rows and
+ *   (batch-1)*stride_out + rows <= ld_out.  Otherwise DESC_ERR_SHAPE.  Input matrices may overlap (read-only).  Strides must be >= 0.
  *   The caller owns both buffers; the library allocates no device memory and
  *   keeps only a host-side, thread-safe cache of TMA descriptors.
  *
  * Memory space.
- *   Both pointers must be device (or managed) memory of the CURRENT device
- *   (cudaPointerGetAttributes), else DESC_ERR_MEMSPACE.  desc_transpose_host is
- *   the one entry point that takes host buffers.
+ *   Both pointers must be device (or managed) memory of the CURRENT device, or of a
+ *   peer device the current device can access (an IPC-mapped slab of another rank,
+ *   desc_ipc_open), checked with cudaPointerGetAttributes, else DESC_ERR_MEMSPACE.
+ *   desc_transpose_host is the one entry point that takes host buffers.
  *
  * Launch configuration.  Derived inside the library from the shape
  *   and the device's SM count: the caller passes no grid or block sizes, so the
@@ -141,6 +143,27 @@ desc_status desc_transpose_host(const void *h_in, void *h_out, int64_t batch,
                                 int64_t ld_out, int64_t stride_in,
                                 int64_t stride_out, desc_dtype dtype, void *d_work,
                                 size_t work_bytes, void *stream);
+
+/* Strided batched copy, NO transposition:  out[b][i][j] = in[b][i][j]
+ * (in: rows x cols, pitch ld_in >= cols; out: rows x cols, pitch ld_out >= cols; batch
+ * strides as above).  The unpack step of the distributed slab transpose
+ * (paper_2305_03448_b200/dist.py): P received R x R blocks placed side by side in the
+ * output slab.  Same ownership / memory-space / error rules as desc_transpose_batched
+ * (output matrices pairwise disjoint: stacked, stride_out >= (rows-1)*ld_out + cols,
+ * or side by side, stride_out >= cols and (batch-1)*stride_out + cols <= ld_out). */
+desc_status desc_copy_batched(const void *in, void *out, int64_t batch, int64_t rows,
+                              int64_t cols, int64_t ld_in, int64_t ld_out,
+                              int64_t stride_in, int64_t stride_out, desc_dtype dtype,
+                              void *stream);
+
+/* CUDA IPC plumbing for the fused peer-to-peer distributed transpose (dist.py):
+ * export a device allocation as a DESC_IPC_HANDLE_BYTES-byte handle, map a peer's
+ * handle into this process (peer access enabled lazily), unmap it.  Errors:
+ * DESC_ERR_NULL, DESC_ERR_CUDA. */
+#define DESC_IPC_HANDLE_BYTES 64
+desc_status desc_ipc_handle(const void *dptr, void *handle_out);
+desc_status desc_ipc_open(const void *handle, void **dptr_out);
+desc_status desc_ipc_close(void *dptr);
 
 /* Recommended workspace bytes for desc_transpose_host (double-buffered 1024-row bands). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);

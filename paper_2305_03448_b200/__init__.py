@@ -20,7 +20,8 @@ __all__ = [
     "DescError", "DTYPE", "KERNEL", "lib_path", "load",
     "desc_transpose", "desc_transpose_batched", "desc_transpose_ex", "desc_select_kernel",
     "desc_status_string", "desc_last_error", "desc_dtype_size", "desc_version",
-    "desc_last_launch_count", "desc_transpose_host", "desc_transpose_host_workspace",
+    "desc_last_launch_count", "desc_copy_batched", "desc_transpose_host",
+    "desc_ipc_handle", "desc_ipc_open", "desc_ipc_close", "desc_transpose_host_workspace",
     "transpose", "transpose_batched", "transpose_host",
 ]
 
@@ -68,6 +69,14 @@ def load():
     lib.desc_transpose_host.restype = ci
     lib.desc_transpose_host_workspace.argtypes = [i64, i64, ci]
     lib.desc_transpose_host_workspace.restype = ctypes.c_size_t
+    lib.desc_copy_batched.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci, vp]
+    lib.desc_copy_batched.restype = ci
+    lib.desc_ipc_handle.argtypes = [vp, vp]
+    lib.desc_ipc_handle.restype = ci
+    lib.desc_ipc_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
+    lib.desc_ipc_open.restype = ci
+    lib.desc_ipc_close.argtypes = [vp]
+    lib.desc_ipc_close.restype = ci
     lib.desc_last_launch_count.argtypes = []
     lib.desc_last_launch_count.restype = ci
     lib.desc_status_string.argtypes = [ci]
@@ -124,6 +133,33 @@ def desc_transpose_host(h_in_ptr, h_out_ptr, batch, rows, cols, ld_in, ld_out, s
 
 def desc_transpose_host_workspace(rows, cols, dtype) -> int:
     return load().desc_transpose_host_workspace(rows, cols, _dt(dtype))
+
+
+def desc_copy_batched(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
+                      dtype, stream=0):
+    return _check(load().desc_copy_batched(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out,
+                                           stride_in, stride_out, _dt(dtype), stream))
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def desc_ipc_handle(dptr) -> bytes:
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(load().desc_ipc_handle(dptr, buf))
+    return buf.raw
+
+
+def desc_ipc_open(handle: bytes) -> int:
+    if len(handle) != IPC_HANDLE_BYTES:
+        raise ValueError("IPC handle must be 64 bytes")
+    p = ctypes.c_void_p()
+    _check(load().desc_ipc_open(handle, ctypes.byref(p)))
+    return p.value
+
+
+def desc_ipc_close(dptr) -> None:
+    _check(load().desc_ipc_close(dptr))
 
 
 def desc_status_string(status: int) -> str:

@@ -1,0 +1,38 @@
+// copy_kernel.cuh -- strided batched block copy  out[b][i][j] = in[b][i][j].
+//
+// The untransposed "unpack" step of the distributed slab transpose (BASELINE.json
+// north_star (4)): the all-to-all delivers P contiguous R x R blocks that
+// must land side by side (pitch N) in the output slab.  In the paper's terms it is the
+// identity view applied to a `group`-ed place (Listing 3) -- a copy between
+// two layouts of the same elements, no transposition.
+//
+// One CTA per row (grid-stride over batch*rows rows), threads stride over 16-byte (or
+// element-sized) units of the row, 4 units in flight per thread.
+#pragma once
+#include <cstdint>
+
+namespace desc {
+
+template <typename V>
+__global__ void __launch_bounds__(256)
+copy_rows_kernel(const char *__restrict__ in, char *__restrict__ out, int64_t rows,
+                 int64_t total_rows, int64_t units, int64_t ld_in_b, int64_t ld_out_b,
+                 int64_t stride_in_b, int64_t stride_out_b) {
+    for (int64_t r = blockIdx.x; r < total_rows; r += gridDim.x) {
+        const int64_t b = r / rows, i = r - b * rows;
+        const V *src = reinterpret_cast<const V *>(in + b * stride_in_b + i * ld_in_b);
+        V *dst = reinterpret_cast<V *>(out + b * stride_out_b + i * ld_out_b);
+        int64_t u = threadIdx.x;
+        for (; u + 3 * blockDim.x < units; u += 4 * blockDim.x) {
+            const V v0 = src[u], v1 = src[u + blockDim.x], v2 = src[u + 2 * blockDim.x],
+                    v3 = src[u + 3 * blockDim.x];
+            dst[u] = v0;
+            dst[u + blockDim.x] = v1;
+            dst[u + 2 * blockDim.x] = v2;
+            dst[u + 3 * blockDim.x] = v3;
+        }
+        for (; u < units; u += blockDim.x) dst[u] = src[u];
+    }
+}
+
+}  // namespace desc

@@ -18,6 +18,7 @@
 #include "smem_transpose.cuh"
 #include "tma_transpose.cuh"
 #include "tma_store_transpose.cuh"
+#include "copy_kernel.cuh"
 
 namespace {
 
@@ -61,6 +62,21 @@ bool span_elems(int64_t batch, int64_t nr, int64_t nc, int64_t ld, int64_t strid
     if (!add_ok(a, b, &s) || !add_ok(s, nc, &s)) return false;
     *out = s;
     return true;
+}
+
+// Are `batch` output matrices of `nr` rows x `nc` cols (pitch ld, batch stride) pairwise
+// disjoint?  Two layouts are accepted (the narrowing rule: each batch item
+// uniquely owns its part of out): stacked (stride >= (nr-1)*ld + nc) and side by side
+// within each row (stride >= nc and (batch-1)*stride + nc <= ld).
+bool outputs_disjoint(int64_t batch, int64_t nr, int64_t nc, int64_t ld, int64_t stride) {
+    if (batch <= 1) return true;
+    int64_t span;
+    if (span_elems(1, nr, nc, ld, 0, &span) && stride >= span) return true;
+    int64_t last;
+    if (stride >= nc && !__builtin_mul_overflow(batch - 1, stride, &last) &&
+        !__builtin_add_overflow(last, nc, &last) && last <= ld)
+        return true;
+    return false;
 }
 
 struct Args {
@@ -449,9 +465,16 @@ desc_status check_memspace(const void *p, int dev, const char *name) {
     if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
         return fail(DESC_ERR_MEMSPACE, "%s is not device memory (cudaMemoryType %d)", name,
                     (int)attr.type);
-    if (attr.type == cudaMemoryTypeDevice && attr.device != dev)
-        return fail(DESC_ERR_MEMSPACE, "%s lives on device %d, current device is %d", name,
-                    attr.device, dev);
+    if (attr.type == cudaMemoryTypeDevice && attr.device != dev) {
+        // peer memory (e.g. an IPC-mapped slab of another rank, dist.py): allowed when the
+        // current device can access the owning device over NVLink / PCIe
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, dev, attr.device) != cudaSuccess || !can) {
+            cudaGetLastError();
+            return fail(DESC_ERR_MEMSPACE, "%s lives on device %d, not accessible from device %d",
+                        name, attr.device, dev);
+        }
+    }
     return DESC_OK;
 }
 
@@ -466,14 +489,13 @@ desc_status validate(const Args &a, bool *empty) {
     if (a.ld_in < a.cols) return fail(DESC_ERR_SHAPE, "ld_in %lld < cols %lld", (long long)a.ld_in, (long long)a.cols);
     if (a.ld_out < a.rows) return fail(DESC_ERR_SHAPE, "ld_out %lld < rows %lld", (long long)a.ld_out, (long long)a.rows);
     if (a.stride_in < 0 || a.stride_out < 0) return fail(DESC_ERR_SHAPE, "negative batch stride");
-    if (a.batch > 1) {
-        int64_t need;
-        if (!span_elems(1, a.cols, a.rows, a.ld_out, 0, &need))
-            return fail(DESC_ERR_SHAPE, "output matrix extent overflows int64");
-        if (a.stride_out < need)
-            return fail(DESC_ERR_SHAPE,
-                        "batched outputs overlap: stride_out %lld < (cols-1)*ld_out+rows = %lld",
-                        (long long)a.stride_out, (long long)need);
+    if (!outputs_disjoint(a.batch, a.cols, a.rows, a.ld_out, a.stride_out)) {
+        int64_t need = 0;
+        span_elems(1, a.cols, a.rows, a.ld_out, 0, &need);
+        return fail(DESC_ERR_SHAPE,
+                        "batched outputs overlap: stride_out %lld is neither >= (cols-1)*ld_out+rows"
+                    " = %lld nor a side-by-side layout within ld_out",
+                    (long long)a.stride_out, (long long)need);
     }
     int64_t span_in, span_out, bin, bout;
     if (!span_elems(a.batch, a.rows, a.cols, a.ld_in, a.stride_in, &span_in) ||
@@ -580,7 +602,7 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     if (!h_in || !h_out || !d_work) return fail(DESC_ERR_NULL, "null pointer");
     if (ld_in < cols || ld_out < rows) return fail(DESC_ERR_SHAPE, "ld smaller than the row extent");
     if (stride_in < 0 || stride_out < 0) return fail(DESC_ERR_SHAPE, "negative batch stride");
-    if (batch > 1 && stride_out < (cols - 1) * ld_out + rows)
+    if (!outputs_disjoint(batch, cols, rows, ld_out, stride_out))
         return fail(DESC_ERR_SHAPE, "batched outputs overlap");
     int64_t span_in, span_out, bin, bout;
     if (!span_elems(batch, rows, cols, ld_in, stride_in, &span_in) ||
@@ -651,9 +673,73 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     return DESC_OK;
 }
 
+// ---- strided batched copy (desc_copy_batched) -----------------------------------------
+desc_status run_copy(const void *in, void *out, int64_t batch, int64_t rows, int64_t cols,
+                     int64_t ld_in, int64_t ld_out, int64_t stride_in, int64_t stride_out, int es,
+                     cudaStream_t stream) {
+    g_last_launches = 0;
+    if (es == 0) return fail(DESC_ERR_DTYPE, "unknown dtype");
+    if (batch < 0 || rows < 0 || cols < 0) return fail(DESC_ERR_SHAPE, "negative size");
+    if (batch == 0 || rows == 0 || cols == 0) return DESC_OK;
+    if (!in || !out) return fail(DESC_ERR_NULL, "null %s pointer", in ? "out" : "in");
+    if (ld_in < cols || ld_out < cols) return fail(DESC_ERR_SHAPE, "ld smaller than cols");
+    if (stride_in < 0 || stride_out < 0) return fail(DESC_ERR_SHAPE, "negative batch stride");
+    if (!outputs_disjoint(batch, rows, cols, ld_out, stride_out))
+        return fail(DESC_ERR_SHAPE, "batched outputs overlap");
+    int64_t span_in, span_out, bin, bout;
+    if (!span_elems(batch, rows, cols, ld_in, stride_in, &span_in) ||
+        !span_elems(batch, rows, cols, ld_out, stride_out, &span_out) ||
+        !mul_ok(span_in, es, &bin) || !mul_ok(span_out, es, &bout))
+        return fail(DESC_ERR_SHAPE, "extent overflows int64");
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(in), o0 = reinterpret_cast<uintptr_t>(out);
+    if (i0 < o0 + (uintptr_t)bout && o0 < i0 + (uintptr_t)bin)
+        return fail(DESC_ERR_ALIAS, "in and out overlap (&uniq, P:576-579)");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (desc_status st = check_memspace(in, dev, "in")) return st;
+    if (desc_status st = check_memspace(out, dev, "out")) return st;
+    DevInfo di;
+    if (desc_status st = device_info(dev, &di)) return st;
+    const int64_t total_rows = batch * rows;
+    const int grid = (int)(total_rows < (int64_t)di.sms * 8 ? total_rows : (int64_t)di.sms * 8);
+    const bool vec16 = (i0 % 16 == 0) && (o0 % 16 == 0) && (cols * es) % 16 == 0 &&
+                       (ld_in * es) % 16 == 0 && (ld_out * es) % 16 == 0 &&
+                       (batch == 1 || ((stride_in * es) % 16 == 0 && (stride_out * es) % 16 == 0));
+    const char *ci = static_cast<const char *>(in);
+    char *co = static_cast<char *>(out);
+    const int64_t sib = batch > 1 ? stride_in * es : 0, sob = batch > 1 ? stride_out * es : 0;
+    if (vec16)
+        desc::copy_rows_kernel<uint4><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols * es / 16,
+                                                               ld_in * es, ld_out * es, sib, sob);
+    else if (es == 8)
+        desc::copy_rows_kernel<unsigned long long><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+                                                                            ld_in * es, ld_out * es, sib, sob);
+    else if (es == 4)
+        desc::copy_rows_kernel<uint32_t><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+                                                                  ld_in * es, ld_out * es, sib, sob);
+    else if (es == 2)
+        desc::copy_rows_kernel<uint16_t><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+                                                                  ld_in * es, ld_out * es, sib, sob);
+    else
+        desc::copy_rows_kernel<uint8_t><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+                                                                 ld_in * es, ld_out * es, sib, sob);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "copy_rows_kernel launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+desc_status desc_copy_batched(const void *in, void *out, int64_t batch, int64_t rows, int64_t cols,
+                              int64_t ld_in, int64_t ld_out, int64_t stride_in,
+                              int64_t stride_out, desc_dtype dtype, void *stream) {
+    return run_copy(in, out, batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
+                    dtype_size(dtype), static_cast<cudaStream_t>(stream));
+}
 
 desc_status desc_transpose_ex(const void *in, void *out, int64_t batch, int64_t rows, int64_t cols,
                               int64_t ld_in, int64_t ld_out, int64_t stride_in, int64_t stride_out,
@@ -698,6 +784,32 @@ size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtyp
     if (es == 0 || rows <= 0 || cols <= 0) return 0;
     const int64_t band = rows < 1024 ? rows : 1024;
     return (size_t)band_bytes(band, cols, es);
+}
+
+desc_status desc_ipc_handle(const void *dptr, void *handle_out) {
+    if (!dptr || !handle_out) return fail(DESC_ERR_NULL, "null pointer");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dptr));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == DESC_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle_out, &h, sizeof(h));
+    return DESC_OK;
+}
+
+desc_status desc_ipc_open(const void *handle, void **dptr_out) {
+    if (!handle || !dptr_out) return fail(DESC_ERR_NULL, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    return DESC_OK;
+}
+
+desc_status desc_ipc_close(void *dptr) {
+    if (!dptr) return fail(DESC_ERR_NULL, "null pointer");
+    cudaError_t e = cudaIpcCloseMemHandle(dptr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+    return DESC_OK;
 }
 
 int desc_last_launch_count(void) { return g_last_launches; }

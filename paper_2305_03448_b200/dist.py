@@ -1,0 +1,185 @@
+"""Distributed transpose of a row-slab-sharded matrix across the GPUs of one node.
+
+BASELINE.json north_star (4) / SURVEY.md §8(a) a9, §8(e).  The paper has no multi-GPU
+content; this is the build's extension of the transpose (reading R13):
+
+  global input A is M x N, rank r of P owns input rows  [r*Rm, (r+1)*Rm),  Rm = M / P
+  global output A^T is N x M, rank r owns output rows   [r*Rn, (r+1)*Rn),  Rn = N / P
+  block (r, s) = A[r*Rm:(r+1)*Rm, s*Rn:(s+1)*Rn] travels to rank s, transposed, and lands
+  at out_s[:, r*Rm:(r+1)*Rm].
+
+Two implementations:
+
+* ``slab_transpose`` -- NCCL path (the baseline the north star names):
+    1. local transpose of the whole slab (desc kernel): T_r = in_r^T is N x Rm, and its row
+       band s (rows s*Rn..) is exactly block (r, s)^T, contiguous -> the all-to-all send buffer;
+    2. ``all_to_all_single`` over NCCL (NVLink 5 / NVSwitch);
+    3. unpack: the P received Rn x Rm blocks are placed side by side in out_r with
+       ``desc_copy_batched`` (pitch M).
+  Per-rank HBM traffic ~6 S (S = slab bytes), NVLink S (P-1)/P each direction.
+
+* ``PeerSlabTranspose`` -- fused peer-to-peer path: every rank maps the
+  other ranks' output slabs with CUDA IPC once; a call launches the TMA transpose kernel
+  per destination block, writing block (r, s)^T straight into out_s over NVLink -- one pass,
+  no pack/unpack, no NCCL kernels: HBM 2 S per rank (read local S, the writes of S land in
+  the peers' HBM), NVLink S (P-1)/P.  A group barrier after the kernels orders the writes
+  before anyone reads its slab.
+
+The local steps are injectable (``local_transpose``/``local_copy``) only so the exchange
+logic can be tested on CPU with the gloo backend (tests/test_dist_cpu.py); the product
+default is the CUDA library, and CUDA tensors are required.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+import paper_2305_03448_b200 as desc
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    M: int          # global rows of the input
+    N: int          # global cols of the input
+    P: int          # ranks
+    r: int          # this rank
+
+    def __post_init__(self):
+        if self.P < 1 or not (0 <= self.r < self.P):
+            raise ValueError("bad rank / world size")
+        if self.M % self.P or self.N % self.P:
+            raise ValueError(f"M={self.M} and N={self.N} must both divide by P={self.P} (R13)")
+
+    @property
+    def Rm(self) -> int:
+        return self.M // self.P
+
+    @property
+    def Rn(self) -> int:
+        return self.N // self.P
+
+    def in_rows(self, r=None):
+        r = self.r if r is None else r
+        return r * self.Rm, (r + 1) * self.Rm
+
+    def out_rows(self, r=None):
+        r = self.r if r is None else r
+        return r * self.Rn, (r + 1) * self.Rn
+
+    def algorithmic_bytes(self, es: int) -> int:
+        """Bytes the method must move per rank: read the slab, write the slab."""
+        return 2 * self.Rm * self.N * es
+
+    def nvlink_bytes(self, es: int) -> int:
+        """Bytes per rank that must cross NVLink in each direction: S (P-1)/P."""
+        return self.Rm * self.N * es * (self.P - 1) // self.P
+
+
+def _cuda_transpose(src, dst):
+    """dst (N x Rm) = src (Rm x N)^T with the desc kernels."""
+    desc.transpose(src, dst)
+
+
+def _cuda_unpack(recv, out, P, Rn, Rm, M):
+    """out[:, s*Rm:(s+1)*Rm] = recv[s] for s < P  (recv: P x Rn x Rm contiguous)."""
+    desc.desc_copy_batched(recv.data_ptr(), out.data_ptr(), P, Rn, Rm, Rm, M, Rn * Rm, Rm,
+                           recv.dtype, torch.cuda.current_stream(recv.device).cuda_stream)
+
+
+def slab_transpose(in_slab: torch.Tensor, out_slab: torch.Tensor | None = None, group=None,
+                   local_transpose=None, local_copy=None, workspace=None):
+    """Transpose the global matrix whose row slab this rank holds (NCCL all-to-all path).
+
+    in_slab: (Rm, N) contiguous, this rank's rows of the M x N input (M = Rm * P).
+    returns out_slab: (Rn, M), this rank's rows of the N x M transpose (Rn = N / P).
+    workspace: optional (send, recv) pair of tensors with N * Rm elements each."""
+    P = dist.get_world_size(group) if dist.is_initialized() else 1
+    r = dist.get_rank(group) if dist.is_initialized() else 0
+    Rm, N = in_slab.shape
+    lay = SlabLayout(Rm * P, N, P, r)
+    Rn, M = lay.Rn, lay.M
+    if not in_slab.is_contiguous():
+        raise ValueError("in_slab must be contiguous")
+    if out_slab is None:
+        out_slab = torch.empty((Rn, M), dtype=in_slab.dtype, device=in_slab.device)
+    if tuple(out_slab.shape) != (Rn, M):
+        raise ValueError(f"out_slab must be {(Rn, M)}")
+    local_transpose = local_transpose or _cuda_transpose
+    local_copy = local_copy or _cuda_unpack
+    if P == 1:
+        local_transpose(in_slab, out_slab)
+        return out_slab
+    if workspace is None:
+        send = torch.empty((N, Rm), dtype=in_slab.dtype, device=in_slab.device)
+        recv = torch.empty((P, Rn, Rm), dtype=in_slab.dtype, device=in_slab.device)
+    else:
+        send, recv = workspace
+        send, recv = send.view(N, Rm), recv.view(P, Rn, Rm)
+    local_transpose(in_slab, send)                       # T_r = in_r^T; band s = block (r, s)^T
+    dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+    local_copy(recv, out_slab, P, Rn, Rm, M)             # out_r[:, s*Rm:(s+1)*Rm] = recv[s]
+    return out_slab
+
+
+class PeerSlabTranspose:
+    """Fused peer-to-peer slab transpose over CUDA IPC (one kernel pass, no NCCL kernels).
+
+    Construct once per output slab (collective over `group`): it exports this rank's output
+    slab and maps every peer's.  ``__call__(in_slab)`` then writes block (r, s)^T straight into
+    rank s's slab for every s and finishes with a group barrier (all writes complete before
+    any rank reads its slab).  Works with any process-group backend for the handle exchange
+    (gloo in the single-GPU two-process test, NCCL in bench.py)."""
+
+    def __init__(self, out_slab: torch.Tensor, M: int, group=None, kernel: str = "auto"):
+        if not out_slab.is_cuda or not out_slab.is_contiguous():
+            raise ValueError("out_slab must be a contiguous CUDA tensor")
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        self.out = out_slab
+        self.M = M
+        self.kernel = kernel
+        Rn = out_slab.shape[0]
+        self.lay = SlabLayout(M, Rn * self.P, self.P, self.r)
+        handle = desc.desc_ipc_handle(out_slab.data_ptr())
+        handles = [None] * self.P
+        dist.all_gather_object(handles, (handle, out_slab.data_ptr()), group=group)
+        self.peer_ptr = []
+        self._opened = []
+        for s, (h, ptr) in enumerate(handles):
+            if s == self.r:
+                self.peer_ptr.append(out_slab.data_ptr())
+            else:
+                p = desc.desc_ipc_open(h)
+                self.peer_ptr.append(p)
+                self._opened.append(p)
+
+    def __call__(self, in_slab: torch.Tensor, barrier: bool = True):
+        lay = self.lay
+        Rm, N = in_slab.shape
+        if (Rm, N) != (lay.Rm, lay.N) or not in_slab.is_contiguous():
+            raise ValueError(f"in_slab must be contiguous {(lay.Rm, lay.N)}")
+        es = in_slab.element_size()
+        stream = torch.cuda.current_stream(in_slab.device).cuda_stream
+        if barrier:       # every peer finished reading its previous output
+            dist.barrier(group=self.group)
+        launches = 0
+        # start with the next rank so that the P writers spread over the P destinations
+        for k in range(self.P):
+            s = (self.r + k) % self.P
+            src = in_slab.data_ptr() + s * lay.Rn * es                       # block (r, s)
+            dst = self.peer_ptr[s] + self.r * lay.Rm * es                    # out_s[:, r*Rm]
+            desc.desc_transpose_ex(src, dst, 1, lay.Rm, lay.Rn, lay.N, lay.M, 0, 0,
+                                   in_slab.dtype, self.kernel, stream)
+            launches += desc.desc_last_launch_count()
+        if barrier:
+            torch.cuda.current_stream(in_slab.device).synchronize()
+            dist.barrier(group=self.group)
+        return self.out, launches
+
+    def close(self):
+        for p in self._opened:
+            desc.desc_ipc_close(p)
+        self._opened = []

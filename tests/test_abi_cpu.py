@@ -93,6 +93,11 @@ def test_validation_codes(lib):
     assert _status("desc_transpose", i, o, 1 << 40, 1 << 40, 1 << 40, 1 << 40, 0, None) == 2
     # batched outputs must be disjoint (narrowing)
     assert _status("desc_transpose_batched", i, o, 2, 4, 8, 8, 4, 32, 31, 0, None) == 2
+    # side-by-side batched outputs are disjoint too (the distributed unpack layout)
+    assert _status("desc_transpose_batched", i, o, 2, 4, 8, 8, 8, 32, 4, 0, None) in (5, 6)
+    assert _status("desc_transpose_batched", i, o, 2, 4, 8, 8, 8, 32, 3, 0, None) == 2
+    assert _status("desc_copy_batched", i, o, 4, 8, 16, 16, 64, 128, 16, 0, None) in (5, 6)
+    assert _status("desc_copy_batched", i, o, 4, 8, 16, 16, 63, 128, 16, 0, None) == 2
     # dtype
     assert _status("desc_transpose", i, o, 4, 4, 4, 4, 42, None) == 3
     # aliasing: &uniq out overlapping & in

@@ -1,0 +1,92 @@
+"""Host-side tests of the distributed slab transpose (no GPU): partition math, a fake-ranks
+simulation of the exchange, and the real torch.distributed code path at world size 2 and 4
+over gloo, with the local steps supplied on the CPU by the ORACLE (test infrastructure) so
+that only the exchange logic of paper_2305_03448_b200/dist.py is under test here.  The CUDA
+local steps are covered by tests/test_gpu_parity.py and tests/test_dist_gpu.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2305_03448_b200 import dist as ddist
+
+
+def test_layout_math():
+    lay = ddist.SlabLayout(65536, 65536, 8, 3)
+    assert (lay.Rm, lay.Rn) == (8192, 8192)
+    assert lay.in_rows() == (3 * 8192, 4 * 8192) and lay.out_rows(7) == (7 * 8192, 65536)
+    assert lay.algorithmic_bytes(4) == 2 * 8192 * 65536 * 4
+    assert lay.nvlink_bytes(4) == 8192 * 65536 * 4 * 7 // 8
+    with pytest.raises(ValueError):
+        ddist.SlabLayout(100, 64, 8, 0)       # R13: P must divide both dimensions
+    with pytest.raises(ValueError):
+        ddist.SlabLayout(64, 64, 4, 4)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("shape", [(64, 64), (32, 96), (128, 40)])
+def test_fake_ranks_exchange(P, shape):
+    """The three steps of slab_transpose simulated with P numpy ranks and an in-memory
+    all-to-all reproduce the oracle's global transpose, slab by slab."""
+    M, N = shape
+    if M % P or N % P:
+        pytest.skip("P must divide M and N")
+    A = synth.random_bits((M, N), 4, M * N + P)
+    Rm, Rn = M // P, N // P
+    sends = [oracle.transpose(A[r * Rm:(r + 1) * Rm]) for r in range(P)]        # step 1
+    recvs = [np.stack([sends[s][r * Rn:(r + 1) * Rn] for s in range(P)]) for r in range(P)]
+    for r in range(P):                                                            # step 3
+        out = np.empty((Rn, M), dtype=A.dtype)
+        for s in range(P):
+            out[:, s * Rm:(s + 1) * Rm] = recvs[r][s]
+        assert out.tobytes() == oracle.dist_expected_slab(A, r, P).tobytes()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _cpu_transpose(src, dst):           # oracle-backed local step (test only)
+    dst.copy_(torch.from_numpy(oracle.transpose(src.numpy())))
+
+
+def _cpu_unpack(recv, out, P, Rn, Rm, M):
+    for s in range(P):
+        out[:, s * Rm:(s + 1) * Rm] = recv[s]
+
+
+def _worker(rank, world, port, M, N, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.random_bits((M, N), 4, 1234)         # every rank can build the global input
+        Rm = M // world
+        slab = torch.from_numpy(A[rank * Rm:(rank + 1) * Rm].view(np.int32).copy())
+        out = ddist.slab_transpose(slab, local_transpose=_cpu_transpose, local_copy=_cpu_unpack)
+        ok = out.numpy().view(np.uint32).tobytes() == oracle.dist_expected_slab(A, rank, world).tobytes()
+        q.put((rank, ok))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,M,N", [(2, 64, 96), (4, 128, 64)])
+def test_gloo_slab_transpose(world, M, N):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}

@@ -1,0 +1,102 @@
+"""GPU tests of the distributed-transpose building blocks on ONE B200 (the only GPU gpurun
+gives): the unpack copy kernel, side-by-side batched outputs, the P = 1 slab transpose, and
+the fused peer-to-peer path with two processes that share cuda:0 (CUDA IPC works between
+processes on the same device; the process group is gloo, used only for the IPC-handle
+exchange and the barriers).  Every result is compared with the CPU oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+import paper_2305_03448_b200 as desc
+from paper_2305_03448_b200 import dist as ddist
+
+pytestmark = pytest.mark.gpu
+
+
+def test_copy_batched_side_by_side():
+    """desc_copy_batched: P blocks (Rn x Rm) -> side by side in an Rn x (P*Rm) slab."""
+    for P, Rn, Rm, es in ((4, 64, 96, 4), (8, 33, 17, 8), (2, 128, 256, 4)):
+        blocks = synth.random_bits((P, Rn, Rm), es, P * Rn + Rm)
+        it = {4: np.int32, 8: np.int64}[es]
+        recv = torch.from_numpy(blocks.view(it)).cuda()
+        out = torch.full((Rn, P * Rm), -1, dtype=recv.dtype, device="cuda")
+        desc.desc_copy_batched(recv.data_ptr(), out.data_ptr(), P, Rn, Rm, Rm, P * Rm, Rn * Rm, Rm,
+                               "f32" if es == 4 else "f64", torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(blocks.dtype),
+                              np.concatenate(list(blocks), axis=1))
+
+
+def test_transpose_batched_side_by_side_outputs():
+    """Batched transpose whose outputs sit side by side (receive-side unpack-by-transpose)."""
+    P, R = 4, 96
+    blocks = synth.random_bits((P, R, R), 4, 5)
+    x = torch.from_numpy(blocks.view(np.int32)).cuda()
+    out = torch.empty((R, P * R), dtype=torch.int32, device="cuda")
+    desc.desc_transpose_batched(x.data_ptr(), out.data_ptr(), P, R, R, R, P * R, R * R, R, "i32",
+                                torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    exp = np.concatenate([oracle.transpose(b) for b in blocks], axis=1)
+    assert out.cpu().numpy().view(np.uint32).tobytes() == exp.tobytes()
+
+
+def test_slab_transpose_single_rank():
+    A = synth.random_bits((512, 768), 4, 8)
+    x = torch.from_numpy(A.view(np.int32)).cuda()
+    y = ddist.slab_transpose(x)
+    torch.cuda.synchronize()
+    assert y.cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(A).tobytes()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _p2p_worker(rank, world, port, M, N, es, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.random_bits((M, N), es, 77)
+        it = {4: np.int32, 8: np.int64}[es]
+        Rm, Rn = M // world, N // world
+        slab = torch.from_numpy(A[rank * Rm:(rank + 1) * Rm].view(it).copy()).cuda()
+        out = torch.full((Rn, M), -1, dtype=slab.dtype, device="cuda")
+        xp = ddist.PeerSlabTranspose(out, M)
+        ok = True
+        for _ in range(2):        # twice: the exported slabs are reusable
+            got, launches = xp(slab)
+            ok &= launches == world
+            ok &= got.cpu().numpy().view(A.dtype).tobytes() == \
+                oracle.dist_expected_slab(A, rank, world).tobytes()
+        xp.close()
+        q.put((rank, bool(ok)))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,M,N,es", [(2, 512, 768, 4), (2, 640, 256, 8), (4, 256, 512, 4)])
+def test_peer_slab_transpose_two_processes_one_gpu(world, M, N, es):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, M, N, es, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}
