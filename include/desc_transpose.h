@@ -157,11 +157,13 @@ desc_status desc_copy_batched(const void *in, void *out, int64_t batch, int64_t 
                               void *stream);
 
 /* CUDA IPC plumbing for the fused peer-to-peer distributed transpose (dist.py):
- * export a device allocation as a DESC_IPC_HANDLE_BYTES-byte handle, map a peer's
- * handle into this process (peer access enabled lazily), unmap it.  Errors:
- * DESC_ERR_NULL, DESC_ERR_CUDA. */
+ * desc_ipc_handle exports the allocation containing dptr as a DESC_IPC_HANDLE_BYTES-byte
+ * handle plus dptr's byte offset inside that allocation; desc_ipc_open maps a peer's
+ * handle into this process (peer access enabled lazily) and returns the allocation BASE
+ * (add the exported offset); desc_ipc_close unmaps it.  Errors: DESC_ERR_NULL,
+ * DESC_ERR_CUDA. */
 #define DESC_IPC_HANDLE_BYTES 64
-desc_status desc_ipc_handle(const void *dptr, void *handle_out);
+desc_status desc_ipc_handle(const void *dptr, void *handle_out, uint64_t *offset_out);
 desc_status desc_ipc_open(const void *handle, void **dptr_out);
 desc_status desc_ipc_close(void *dptr);
 

@@ -71,7 +71,7 @@ def load():
     lib.desc_transpose_host_workspace.restype = ctypes.c_size_t
     lib.desc_copy_batched.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci, vp]
     lib.desc_copy_batched.restype = ci
-    lib.desc_ipc_handle.argtypes = [vp, vp]
+    lib.desc_ipc_handle.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
     lib.desc_ipc_handle.restype = ci
     lib.desc_ipc_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
     lib.desc_ipc_open.restype = ci
@@ -144,13 +144,16 @@ def desc_copy_batched(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride_
 IPC_HANDLE_BYTES = 64
 
 
-def desc_ipc_handle(dptr) -> bytes:
+def desc_ipc_handle(dptr):
+    """-> (64-byte handle of the allocation containing dptr, dptr's offset in it)"""
     buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
-    _check(load().desc_ipc_handle(dptr, buf))
-    return buf.raw
+    off = ctypes.c_uint64()
+    _check(load().desc_ipc_handle(dptr, buf, ctypes.byref(off)))
+    return buf.raw, off.value
 
 
 def desc_ipc_open(handle: bytes) -> int:
+    """Map a peer allocation; returns its BASE address (add the exported offset)."""
     if len(handle) != IPC_HANDLE_BYTES:
         raise ValueError("IPC handle must be 64 bytes")
     p = ctypes.c_void_p()

@@ -786,13 +786,30 @@ size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtyp
     return (size_t)band_bytes(band, cols, es);
 }
 
-desc_status desc_ipc_handle(const void *dptr, void *handle_out) {
-    if (!dptr || !handle_out) return fail(DESC_ERR_NULL, "null pointer");
+desc_status desc_ipc_handle(const void *dptr, void *handle_out, uint64_t *offset_out) {
+    if (!dptr || !handle_out || !offset_out) return fail(DESC_ERR_NULL, "null pointer");
+    // the handle names the whole allocation (a caching allocator sub-allocates), so also
+    // report dptr's offset from the allocation base (cuMemGetAddressRange)
+    static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+    });
+    if (!range) return fail(DESC_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    CUresult r = range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr));
+    if (r != CUDA_SUCCESS) return fail(DESC_ERR_CUDA, "cuMemGetAddressRange failed (CUresult %d)", (int)r);
     cudaIpcMemHandle_t h;
-    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dptr));
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
     if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
     static_assert(sizeof(h) == DESC_IPC_HANDLE_BYTES, "IPC handle size");
     memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)(reinterpret_cast<CUdeviceptr>(dptr) - base);
     return DESC_OK;
 }
 

@@ -143,18 +143,18 @@ class PeerSlabTranspose:
         self.kernel = kernel
         Rn = out_slab.shape[0]
         self.lay = SlabLayout(M, Rn * self.P, self.P, self.r)
-        handle = desc.desc_ipc_handle(out_slab.data_ptr())
+        handle, offset = desc.desc_ipc_handle(out_slab.data_ptr())
         handles = [None] * self.P
-        dist.all_gather_object(handles, (handle, out_slab.data_ptr()), group=group)
+        dist.all_gather_object(handles, (handle, offset), group=group)
         self.peer_ptr = []
         self._opened = []
-        for s, (h, ptr) in enumerate(handles):
+        for s, (h, off) in enumerate(handles):
             if s == self.r:
                 self.peer_ptr.append(out_slab.data_ptr())
             else:
-                p = desc.desc_ipc_open(h)
-                self.peer_ptr.append(p)
-                self._opened.append(p)
+                base = desc.desc_ipc_open(h)          # allocation base in this process
+                self.peer_ptr.append(base + off)
+                self._opened.append(base)
 
     def __call__(self, in_slab: torch.Tensor, barrier: bool = True):
         lay = self.lay
