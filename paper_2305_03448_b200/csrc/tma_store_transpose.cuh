@@ -104,6 +104,7 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[STAGES];
     __shared__ __align__(8) uint64_t empty_bar[STAGES];
+    __shared__ int64_t tile_id[STAGES];
 
     const uint32_t in_base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
     const uint32_t out_base = in_base + STAGES * C::STAGE_BYTES;
@@ -128,13 +129,28 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
         if (lane == 0) {
             ptx::prefetch_tensormap(&map_in);
             const uint64_t policy = p.evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
-            int it = 0;
-            for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+            // Tile ids: static round robin, or (p.sched != nullptr) fetched from a global
+            // counter so that faster SMs take more tiles (dynamic scheduling).  The next id
+            // is fetched one tile ahead to hide the atomic's latency.  The id travels to the
+            // consumers through tile_id[s] (published by the full barrier's release).
+            auto fetch = [&](int it) -> int64_t {
+                return p.sched ? (int64_t)atomicAdd(p.sched, 1ull)
+                               : (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+            };
+            int64_t t_next = fetch(0);
+            for (int it = 0;; ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+                const int64_t t = t_next;
+                if (t < p.ntiles) t_next = fetch(it + 1);
                 ptx::mbar_wait(ptx::smem_u32(&empty_bar[s]), ph ^ 1u);
-                const TileCoord tc = tile_coords(t, p);
+                tile_id[s] = t;
                 const uint32_t fb = ptx::smem_u32(&full_bar[s]);
+                if (t >= p.ntiles) {                   // no more work: tell the consumers
+                    ptx::mbar_arrive(fb);
+                    break;
+                }
+                const TileCoord tc = tile_coords(t, p);
                 ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
 #pragma unroll
                 for (int nb = 0; nb < NB; ++nb) {
@@ -144,6 +160,7 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
                     else ptx::tma_load_2d(dst, &map_in, fb, c0, tc.ti * TR, policy);
                 }
             }
+            if (p.sched) sched_release(p);             // this CTA fetched its last id
         }
         return;
     }
@@ -159,11 +176,12 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
         return (((cw + q * CW) % C::TASKS_PER_BOX) % C::CHUNK_GROUPS) * L::CHUNKS_PER_WARP + b_lane;
     };
 
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
         ptx::mbar_wait(ptx::smem_u32(&full_bar[s]), ph);           // TMA bytes landed
+        const int64_t t = tile_id[s];
+        if (t >= p.ntiles) break;
 
         const uint32_t sbase = in_base + s * C::STAGE_BYTES;
         uint4 r[TPW][VEC];

@@ -42,7 +42,21 @@ struct TmaParams {
     int32_t group;       // tile rows per raster group (>= 1), see tile_coords
     int32_t evict_first; // 1 => L2 evict_first hint on the TMA loads
     int64_t ntiles;
+    unsigned long long *sched;  // dynamic tile counter {next, done} (nullptr: static)
 };
+
+// End of a dynamically scheduled launch, called by each CTA's producer thread after it
+// fetched its terminal tile id (it never touches the counter again): the last CTA to check
+// in resets {next, done} for the next launch on the stream, which cannot read the counter
+// before this grid has completed (griddepcontrol.wait / stream order).
+__device__ __forceinline__ void sched_release(const TmaParams &p) {
+    __threadfence();
+    if (atomicAdd(p.sched + 1, 1ull) == gridDim.x - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
+        __threadfence();
+    }
+}
 
 // Linear tile id -> (matrix, tile row, tile col).  Tiles are rastered in groups of
 // `group` tile rows walked column by column, so the tiles in flight at any moment
