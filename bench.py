@@ -135,6 +135,39 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def bench_backend():
+    """Process-group backend: NCCL (one GPU per rank, the driver's launch).  DESC_BENCH_BACKEND=
+    gloo lets several ranks share one GPU to exercise the N > 1 code path on a 1-GPU box
+    (host-side collectives only; the data path never uses a collective here)."""
+    return os.environ.get("DESC_BENCH_BACKEND", "nccl")
+
+
+def init_pg(dev):
+    import torch.distributed as dist
+    if bench_backend() == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(bench_backend())
+
+
+def reduce_scalar(x: float, op: str, dev) -> float:
+    """max/min of a host scalar over ranks (device tensor for NCCL, host tensor for gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64,
+                     device=dev if bench_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.MIN)
+    return float(t.item())
+
+
+def local_device(local: int):
+    import torch
+    n = torch.cuda.device_count()
+    return local % n if bench_backend() != "nccl" else local
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -249,11 +282,12 @@ def ours_arm(args, wl, world, rank, local):
     import torch.distributed as dist
     import paper_2305_03448_b200 as desc
 
+    local = local_device(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     desc.load()
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_pg(dev)
 
     es, rows, cols = wl["es"], wl["rows"], wl["cols"]
     batch = wl["batch"]
@@ -336,10 +370,7 @@ def ours_arm(args, wl, world, rank, local):
         timed_ms = sum(per_launch)
     else:
         timed_ms = region_ms
-    t = torch.tensor([timed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    timed_ms_max = t.item()
+    timed_ms_max = reduce_scalar(timed_ms, "max", dev)
 
     total_bytes = step_bytes * world * args.steps
     value = total_bytes / (timed_ms_max / 1e3) / 1e9
@@ -426,11 +457,12 @@ def dist_arm(args, wl, world, rank, local):
     import paper_2305_03448_b200 as desc
     from paper_2305_03448_b200 import dist as ddist
 
+    local = local_device(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     desc.load()
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_pg(dev)
     M = N = args.dist_n
     es = wl["es"]
     lay = ddist.SlabLayout(M, N, world, rank)
@@ -468,10 +500,7 @@ def dist_arm(args, wl, world, rank, local):
         e1.record(stream)
         torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = t.item()
+    ms_max = reduce_scalar(ms, "max", dev)
     step_s = ms_max / args.steps / 1e3
     total = 2 * M * N * es
     value = total * args.steps / (ms_max / 1e3) / 1e9
@@ -491,9 +520,7 @@ def dist_arm(args, wl, world, rank, local):
         exp = oracle.transpose(synth.hash_expected_np(ii, jj, N, seed, es))
         got = out[j0:j0 + 64, i0:i0 + 64].view(torch.int32).cpu().numpy().view(np.uint32)
         ok &= got.tobytes() == exp.tobytes()
-    okt = torch.tensor([1 if ok else 0], device=dev)
-    if world > 1:
-        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    all_ok = reduce_scalar(1.0 if ok else 0.0, "min", dev) > 0.5
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -514,7 +541,7 @@ def dist_arm(args, wl, world, rank, local):
                          "t_star_ms": round(t_star * 1e3, 4), "t_hbm_ms": round(t_hbm * 1e3, 4),
                          "t_nvlink_ms": round(t_nvl * 1e3, 4), "peak_source": peak_src,
                          "note": "frac = T*/t_step, T* = max(2S/HBM, S(P-1)/P / 770 GB/s)"},
-            "parity": "sampled 64x64 blocks bit-exact vs oracle" if okt.item() else "MISMATCH",
+            "parity": "sampled 64x64 blocks bit-exact vs oracle" if all_ok else "MISMATCH",
             "gpu_launches": launches, "cpu_baseline": None, "e2e": None,
             "clocks": clk.summary(),
         }
@@ -556,11 +583,7 @@ def measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, w
         one()
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = t.item()
+    ms = reduce_scalar(e0.elapsed_time(e1), "max", dev)
     ok = bool(torch.equal(h_out[0, :64, :64], src_t[0, :64, :64].t().contiguous()))
     return {"value": round(2 * nbytes * world * steps / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps,
