@@ -1,7 +1,6 @@
-"""Test-only ground semantics of Descend's basic views (Listing 3,
-P:514-548) and of the paper's two transpose listings, used to PIN the oracle
-against the paper's own worked example.  Not part of the oracle, not part of
-the product.
+"""Test-only simulations of the paper's two transpose listings (Listing 1 thread by
+thread, Listing 2 through the view algebra of Listing 3 -- the basic views come from
+oracle/views.py), used to PIN the oracle against the paper's own worked example.
 
 A view is modelled as an index array: an ndarray whose entries are flat
 offsets into the root array (SPEC S:293-301 `place_index_map` /
@@ -13,34 +12,8 @@ from __future__ import annotations
 import numpy as np
 
 
-# ---- basic views, Listing 3 -------------------------------------
-def group(x: np.ndarray, k: int) -> np.ndarray:
-    """group<k>: [[d;n]] -> [[ [[d;k]]; n/k ]]  (P:517-519, P:537-538; R12: k | n)."""
-    n = x.shape[0]
-    assert n % k == 0, "group: n must be divisible by k (reading R12)"
-    return x.reshape((n // k, k) + x.shape[1:])
-
-
-def transpose(x: np.ndarray) -> np.ndarray:
-    """transpose: [[ [[d;n]]; m ]] -> [[ [[d;m]]; n ]]  -- swaps the OUTER two
-    dims only; d is opaque."""
-    return np.swapaxes(x, 0, 1)
-
-
-def split(x: np.ndarray, k: int):
-    """split<k>: [[d;n]] -> ([[d;k]], [[d;n-k]]) where n >= k."""
-    assert x.shape[0] >= k
-    return x[:k], x[k:]
-
-
-def reverse(x: np.ndarray) -> np.ndarray:
-    """reverse: [[d;n]] -> [[d;n]] reversed (P:521, P:541)."""
-    return x[::-1]
-
-
-def vmap(v, x: np.ndarray) -> np.ndarray:
-    """map(v): applies view v to each element of the outer array."""
-    return np.stack([v(x[i]) for i in range(x.shape[0])])
+# ---- basic views, Listing 3: the oracle's definitions (oracle/views.py) ----
+from oracle.views import group, transpose, split, reverse, vmap  # noqa: E402,F401
 
 
 def group_by_row(x: np.ndarray, row_size: int, num_rows: int) -> np.ndarray:
