@@ -167,6 +167,48 @@ desc_status desc_ipc_handle(const void *dptr, void *handle_out, uint64_t *offset
 desc_status desc_ipc_open(const void *handle, void **dptr_out);
 desc_status desc_ipc_close(void *dptr);
 
+/* ---- view-composed copies (Listing 3) ----
+ * Descend's basic views on a (nested) array: group<k>, transpose (outer two dims), split<k>
+ * (.fst / .snd), reverse; map(v) is encoded as v applied at `depth` = number of enclosing
+ * maps.  A chain of views over a strided root compiles (on the host, no GPU needed) to a
+ * strided view: element v of the view lives at in[offset + sum_d v_d * stride[d]] (strides
+ * in elements, negative after reverse) -- "views are compiled into raw indices"
+ * (P:509-511).  desc_view_copy materialises it: out (contiguous, the view's
+ * row-major order, prod(shape) elements) = the view of `in`.  Views whose innermost dim
+ * transposes onto an input-contiguous dim run on the TMA transpose kernels; the rest on a
+ * row-gather kernel (16-byte vectors when rows are contiguous).  Errors: DESC_ERR_SHAPE for
+ * a view the types of Listing 3 reject (group with k not dividing n -- reading R12; split
+ * with k > n; transpose of a flat array; map deeper than the nesting; > DESC_MAX_DIMS
+ * dims; a view reaching before `in`), plus the usual NULL / DTYPE / ALIAS / MEMSPACE /
+ * CUDA rules.  The caller guarantees the compiled view lies inside the `in` allocation. */
+#define DESC_MAX_DIMS 8
+typedef enum desc_view_kind {
+    DESC_VIEW_GROUP = 0, DESC_VIEW_TRANSPOSE = 1, DESC_VIEW_SPLIT_FST = 2,
+    DESC_VIEW_SPLIT_SND = 3, DESC_VIEW_REVERSE = 4
+} desc_view_kind;
+typedef struct desc_view_op {
+    int32_t kind;   /* desc_view_kind                                  */
+    int32_t depth;  /* number of enclosing map(...) (0 = outermost dim) */
+    int64_t k;      /* nat argument of group / split (ignored otherwise) */
+} desc_view_op;
+typedef struct desc_strided_view {
+    int32_t ndim;
+    int32_t reserved;
+    int64_t offset;                 /* elements                           */
+    int64_t shape[DESC_MAX_DIMS];
+    int64_t stride[DESC_MAX_DIMS];  /* elements, may be negative          */
+} desc_strided_view;
+
+/* Compile a view chain over a root of rank ndim (shape; strides in elements, NULL =
+ * C-contiguous) into *out.  Host only. */
+desc_status desc_view_compile(int32_t ndim, const int64_t *shape, const int64_t *strides,
+                              const desc_view_op *ops, int32_t nops,
+                              desc_strided_view *out);
+
+/* out[0 .. prod(view->shape)) = the view of in, in the view's row-major order. */
+desc_status desc_view_copy(const void *in, void *out, const desc_strided_view *view,
+                           desc_dtype dtype, void *stream);
+
 /* Recommended workspace bytes for desc_transpose_host (double-buffered 1024-row bands). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);
 

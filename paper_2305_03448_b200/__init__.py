@@ -21,7 +21,8 @@ __all__ = [
     "desc_transpose", "desc_transpose_batched", "desc_transpose_ex", "desc_select_kernel",
     "desc_status_string", "desc_last_error", "desc_dtype_size", "desc_version",
     "desc_last_launch_count", "desc_copy_batched", "desc_transpose_host",
-    "desc_ipc_handle", "desc_ipc_open", "desc_ipc_close", "desc_transpose_host_workspace",
+    "desc_ipc_handle", "desc_ipc_open", "desc_ipc_close", "desc_view_compile",
+    "desc_view_copy", "view_copy", "desc_transpose_host_workspace",
     "transpose", "transpose_batched", "transpose_host",
 ]
 
@@ -36,6 +37,23 @@ KERNEL = {"auto": 0, "smem": 1, "tma": 2, "tma_st": 3}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 
 _lib = None
+
+MAX_DIMS = 8
+VIEW_KIND = {"group": 0, "transpose": 1, "split_fst": 2, "split_snd": 3, "reverse": 4}
+
+
+class ViewOp(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("depth", ctypes.c_int32), ("k", ctypes.c_int64)]
+
+
+class StridedView(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("offset", ctypes.c_int64), ("shape", ctypes.c_int64 * MAX_DIMS),
+                ("stride", ctypes.c_int64 * MAX_DIMS)]
+
+    @property
+    def dims(self):
+        return tuple(self.shape[:self.ndim]), tuple(self.stride[:self.ndim]), self.offset
 
 
 class DescError(RuntimeError):
@@ -77,6 +95,12 @@ def load():
     lib.desc_ipc_open.restype = ci
     lib.desc_ipc_close.argtypes = [vp]
     lib.desc_ipc_close.restype = ci
+    lib.desc_view_compile.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ViewOp),
+                                      ctypes.c_int32, ctypes.POINTER(StridedView)]
+    lib.desc_view_compile.restype = ci
+    lib.desc_view_copy.argtypes = [vp, vp, ctypes.POINTER(StridedView), ci, vp]
+    lib.desc_view_copy.restype = ci
     lib.desc_last_launch_count.argtypes = []
     lib.desc_last_launch_count.restype = ci
     lib.desc_status_string.argtypes = [ci]
@@ -139,6 +163,36 @@ def desc_copy_batched(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride_
                       dtype, stream=0):
     return _check(load().desc_copy_batched(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out,
                                            stride_in, stride_out, _dt(dtype), stream))
+
+
+def desc_view_compile(shape, ops, strides=None) -> StridedView:
+    """Compile a view chain [(kind, k, depth), ...] over a root of `shape` (element
+    `strides`, default C-contiguous) into a strided view (host only)."""
+    nd = len(shape)
+    sh = (ctypes.c_int64 * max(nd, 1))(*shape)
+    st = (ctypes.c_int64 * max(nd, 1))(*strides) if strides is not None else None
+    arr = (ViewOp * max(len(ops), 1))(*[ViewOp(VIEW_KIND[k], d, n) for k, n, d in ops])
+    out = StridedView()
+    _check(load().desc_view_compile(nd, sh, st, arr, len(ops), ctypes.byref(out)))
+    return out
+
+
+def desc_view_copy(in_ptr, out_ptr, view: StridedView, dtype, stream=0):
+    return _check(load().desc_view_copy(in_ptr, out_ptr, ctypes.byref(view), _dt(dtype), stream))
+
+
+def view_copy(x, ops, out=None):
+    """Materialise the view chain `ops` of the CUDA tensor x (its own strides are the root's
+    layout): returns a contiguous tensor of the view's shape."""
+    import torch
+    v = desc_view_compile(tuple(x.shape), ops, tuple(x.stride()))
+    shape = v.dims[0]
+    if out is None:
+        out = torch.empty(shape, dtype=x.dtype, device=x.device)
+    if tuple(out.shape) != shape or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous tensor of shape {shape}")
+    desc_view_copy(x.data_ptr(), out.data_ptr(), v, x.dtype, _stream_of(x))
+    return out
 
 
 IPC_HANDLE_BYTES = 64

@@ -19,6 +19,7 @@
 #include "tma_transpose.cuh"
 #include "tma_store_transpose.cuh"
 #include "copy_kernel.cuh"
+#include "view_copy.cuh"
 
 namespace {
 
@@ -778,9 +779,192 @@ desc_status run_copy(const void *in, void *out, int64_t batch, int64_t rows, int
     return DESC_OK;
 }
 
+// ---- views (desc_view_compile / desc_view_copy) -----------------------------------------
+static_assert(DESC_MAX_DIMS == desc::kMaxViewDims, "view rank limits agree");
+
+desc_status view_compile(int32_t ndim, const int64_t *shape, const int64_t *strides,
+                         const desc_view_op *ops, int32_t nops, desc_strided_view *out) {
+    if (!shape || !out || (nops > 0 && !ops)) return fail(DESC_ERR_NULL, "null pointer");
+    if (ndim < 1 || ndim > DESC_MAX_DIMS)
+        return fail(DESC_ERR_SHAPE, "root rank %d outside [1, %d]", ndim, DESC_MAX_DIMS);
+    desc_strided_view v;
+    memset(&v, 0, sizeof v);
+    v.ndim = ndim;
+    for (int d = 0; d < ndim; ++d) {
+        if (shape[d] < 0) return fail(DESC_ERR_SHAPE, "negative extent");
+        v.shape[d] = shape[d];
+    }
+    if (strides) {
+        for (int d = 0; d < ndim; ++d) v.stride[d] = strides[d];
+    } else {                                          // C-contiguous root
+        v.stride[ndim - 1] = 1;
+        for (int d = ndim - 2; d >= 0; --d)
+            if (!mul_ok(v.stride[d + 1], v.shape[d + 1] > 0 ? v.shape[d + 1] : 1, &v.stride[d]))
+                return fail(DESC_ERR_SHAPE, "root extent overflows int64");
+    }
+    for (int i = 0; i < nops; ++i) {
+        const int d = ops[i].depth;
+        const int64_t k = ops[i].k;
+        if (d < 0 || d >= v.ndim)
+            return fail(DESC_ERR_SHAPE, "view %d: map depth %d exceeds the nesting (%d dims)", i, d, v.ndim);
+        const int64_t n = v.shape[d];
+        switch (ops[i].kind) {
+            case DESC_VIEW_GROUP: {                   // [[d;n]] -> [[ [[d;k]]; n/k ]]
+                if (k <= 0 || n % k) return fail(DESC_ERR_SHAPE, "view %d: group<%lld> needs k | n = %lld (R12)", i, (long long)k, (long long)n);
+                if (v.ndim == DESC_MAX_DIMS) return fail(DESC_ERR_SHAPE, "view %d: more than %d dims", i, DESC_MAX_DIMS);
+                for (int e = v.ndim; e > d + 1; --e) { v.shape[e] = v.shape[e - 1]; v.stride[e] = v.stride[e - 1]; }
+                v.shape[d + 1] = k;
+                v.stride[d + 1] = v.stride[d];
+                v.shape[d] = n / k;
+                if (!mul_ok(v.stride[d], k, &v.stride[d])) return fail(DESC_ERR_SHAPE, "stride overflow");
+                ++v.ndim;
+                break;
+            }
+            case DESC_VIEW_TRANSPOSE: {               // swap the outer two dims
+                if (d + 1 >= v.ndim) return fail(DESC_ERR_SHAPE, "view %d: transpose needs a nested array", i);
+                int64_t t = v.shape[d]; v.shape[d] = v.shape[d + 1]; v.shape[d + 1] = t;
+                t = v.stride[d]; v.stride[d] = v.stride[d + 1]; v.stride[d + 1] = t;
+                break;
+            }
+            case DESC_VIEW_SPLIT_FST:                 // ([[d;k]], [[d;n-k]]).fst
+            case DESC_VIEW_SPLIT_SND:
+                if (k < 0 || k > n) return fail(DESC_ERR_SHAPE, "view %d: split<%lld> needs n = %lld >= k", i, (long long)k, (long long)n);
+                if (ops[i].kind == DESC_VIEW_SPLIT_SND) {
+                    v.offset += k * v.stride[d];
+                    v.shape[d] = n - k;
+                } else {
+                    v.shape[d] = k;
+                }
+                break;
+            case DESC_VIEW_REVERSE:
+                if (n > 0) v.offset += (n - 1) * v.stride[d];
+                v.stride[d] = -v.stride[d];
+                break;
+            default:
+                return fail(DESC_ERR_SHAPE, "view %d: unknown kind %d", i, ops[i].kind);
+        }
+    }
+    *out = v;
+    return DESC_OK;
+}
+
+desc_status view_copy(const void *in, void *out, const desc_strided_view *view, int es,
+                      cudaStream_t stream) {
+    g_last_launches = 0;
+    if (es == 0) return fail(DESC_ERR_DTYPE, "unknown dtype");
+    if (!view) return fail(DESC_ERR_NULL, "null view");
+    const desc_strided_view &v = *view;
+    if (v.ndim < 1 || v.ndim > DESC_MAX_DIMS) return fail(DESC_ERR_SHAPE, "view rank outside [1, 8]");
+    int64_t total = 1, lo = v.offset, hi = v.offset;
+    for (int d = 0; d < v.ndim; ++d) {
+        if (v.shape[d] < 0) return fail(DESC_ERR_SHAPE, "negative extent");
+        if (!mul_ok(total, v.shape[d], &total)) return fail(DESC_ERR_SHAPE, "view size overflows int64");
+    }
+    if (total == 0) return DESC_OK;
+    for (int d = 0; d < v.ndim; ++d) {
+        int64_t ext;
+        if (!mul_ok(v.shape[d] - 1, v.stride[d], &ext)) return fail(DESC_ERR_SHAPE, "extent overflow");
+        if (ext < 0) lo += ext; else hi += ext;
+    }
+    if (lo < 0) return fail(DESC_ERR_SHAPE, "view reaches before `in` (offset + negative strides < 0)");
+    if (!in || !out) return fail(DESC_ERR_NULL, "null %s pointer", in ? "out" : "in");
+    int64_t bin_lo, bin_hi, bout;
+    if (!mul_ok(lo, es, &bin_lo) || !mul_ok(hi + 1, es, &bin_hi) || !mul_ok(total, es, &bout))
+        return fail(DESC_ERR_SHAPE, "extent overflows int64");
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(in), o0 = reinterpret_cast<uintptr_t>(out);
+    if (i0 + (uintptr_t)bin_lo < o0 + (uintptr_t)bout && o0 < i0 + (uintptr_t)bin_hi)
+        return fail(DESC_ERR_ALIAS, "view of in and out overlap (&uniq, P:576-579)");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (desc_status st = check_memspace(in, dev, "in")) return st;
+    if (desc_status st = check_memspace(out, dev, "out")) return st;
+
+    // normalise: drop unit dims, merge dims that are contiguous in the input (the output is
+    // the view's own row-major order, so it merges whenever the input does)
+    int nd = 0;
+    int64_t sh[DESC_MAX_DIMS], st_in[DESC_MAX_DIMS];
+    for (int d = 0; d < v.ndim; ++d)
+        if (v.shape[d] != 1) { sh[nd] = v.shape[d]; st_in[nd] = v.stride[d]; ++nd; }
+    if (nd == 0) { sh[0] = 1; st_in[0] = 1; nd = 1; }
+    int m = 0;
+    for (int d = 1; d < nd; ++d) {
+        if (st_in[m] == st_in[d] * sh[d]) { sh[m] *= sh[d]; st_in[m] = st_in[d]; }
+        else { ++m; sh[m] = sh[d]; st_in[m] = st_in[d]; }
+    }
+    nd = m + 1;
+    int64_t st_out[DESC_MAX_DIMS];
+    st_out[nd - 1] = 1;
+    for (int d = nd - 2; d >= 0; --d) st_out[d] = st_out[d + 1] * sh[d + 1];
+    const int L = nd - 1;
+    const char *base = static_cast<const char *>(in) + v.offset * es;
+
+    // transposition of the innermost dim onto an input-contiguous dim: the TMA kernels
+    if (st_in[L] > 1) {
+        int ec = -1, others = 0, b = -1;
+        for (int d = 0; d < L; ++d) {
+            if (st_in[d] == 1 && ec < 0) ec = d;
+            else { ++others; b = d; }
+        }
+        if (ec >= 0 && others <= 1 && (b < 0 || st_in[b] > 0)) {
+            Args a{base, out, b < 0 ? 1 : sh[b], sh[L], sh[ec], st_in[L], st_out[ec],
+                   b < 0 ? 0 : st_in[b], b < 0 ? 0 : st_out[b], es, stream};
+            bool empty;
+            desc_status s = validate(a, &empty);
+            if (s == DESC_OK) return dispatch(a, DESC_KERNEL_AUTO);
+            if (s != DESC_ERR_SHAPE) return s;
+            // geometry the transpose kernels do not take (e.g. interleaved outputs): gather
+        }
+    }
+
+    desc::ViewRows vr;
+    memset(&vr, 0, sizeof vr);
+    vr.outer_ndim = L;
+    for (int d = 0; d < L; ++d) { vr.outer_shape[d] = sh[d]; vr.outer_stride[d] = st_in[d]; }
+    vr.inner = sh[L];
+    vr.inner_stride = st_in[L];
+    vr.offset = v.offset;
+    vr.rows = total / sh[L];
+    DevInfo di;
+    if (desc_status st = device_info(dev, &di)) return st;
+    const int grid = (int)(vr.rows < (int64_t)di.sms * 16 ? vr.rows : (int64_t)di.sms * 16);
+    bool vec = vr.inner_stride == 1 && (i0 % 16 == 0) && (o0 % 16 == 0) &&
+               (v.offset * es) % 16 == 0 && (vr.inner * es) % 16 == 0;
+    for (int d = 0; d < L && vec; ++d) vec = (vr.outer_stride[d] * es) % 16 == 0;
+    if (vec)
+        desc::view_rows_vec_kernel<<<grid, 256, 0, stream>>>(static_cast<const char *>(in),
+                                                             static_cast<char *>(out), vr, es);
+    else if (es == 8)
+        desc::view_rows_kernel<unsigned long long><<<grid, 256, 0, stream>>>(
+            static_cast<const unsigned long long *>(in), static_cast<unsigned long long *>(out), vr);
+    else if (es == 4)
+        desc::view_rows_kernel<uint32_t><<<grid, 256, 0, stream>>>(
+            static_cast<const uint32_t *>(in), static_cast<uint32_t *>(out), vr);
+    else if (es == 2)
+        desc::view_rows_kernel<uint16_t><<<grid, 256, 0, stream>>>(
+            static_cast<const uint16_t *>(in), static_cast<uint16_t *>(out), vr);
+    else
+        desc::view_rows_kernel<uint8_t><<<grid, 256, 0, stream>>>(
+            static_cast<const uint8_t *>(in), static_cast<uint8_t *>(out), vr);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "view_rows_kernel launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+desc_status desc_view_compile(int32_t ndim, const int64_t *shape, const int64_t *strides,
+                              const desc_view_op *ops, int32_t nops, desc_strided_view *out) {
+    return view_compile(ndim, shape, strides, ops, nops, out);
+}
+
+desc_status desc_view_copy(const void *in, void *out, const desc_strided_view *view,
+                           desc_dtype dtype, void *stream) {
+    return view_copy(in, out, view, dtype_size(dtype), static_cast<cudaStream_t>(stream));
+}
 
 desc_status desc_copy_batched(const void *in, void *out, int64_t batch, int64_t rows, int64_t cols,
                               int64_t ld_in, int64_t ld_out, int64_t stride_in,
