@@ -51,6 +51,18 @@ WORKLOADS = {
     "dist65536": dict(batch=1, rows=65536, cols=65536, dtype="f32", es=4, dist=True,
                       name="65536x65536 f32 distributed transpose, row slabs + exchange (BASELINE.json configs[4])"),
 }
+GBT = [("group", 64, 0), ("group", 64, 2), ("transpose", 0, 1)]   # group_by_tile<64,64>
+VIEW_WORKLOADS = {
+    "view_tiles8192f32": ("8192x8192 f32 view copy: group_by_tile<64,64> (tile-major layout)", GBT),
+    "view_transpose8192f32": ("8192x8192 f32 view copy: transpose", [("transpose", 0, 0)]),
+    "view_rot90_8192f32": ("8192x8192 f32 view copy: transpose.map(reverse) (rot90)",
+                           [("transpose", 0, 0), ("reverse", 0, 1)]),
+    "view_flip8192f32": ("8192x8192 f32 view copy: reverse.map(reverse) (rot180)",
+                         [("reverse", 0, 0), ("reverse", 0, 1)]),
+}
+for _k, (_n, _ops) in VIEW_WORKLOADS.items():
+    WORKLOADS[_k] = dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4, view=_ops,
+                         name=_n + " (SURVEY 8(f) NEXT #2)")
 NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU
 
 
@@ -553,6 +565,81 @@ def dist_arm(args, wl, world, rank, local):
     return 0
 
 
+def view_arm(args, wl, world, rank, local):
+    """materialise a view chain of Listing 3 over an 8192^2 f32 root;
+    one step = one desc_view_copy launch; parity vs oracle/views.py materialize."""
+    import torch
+    import paper_2305_03448_b200 as desc
+
+    local = local_device(local)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    desc.load()
+    if world > 1:
+        init_pg(dev)
+    es, rows, cols = wl["es"], wl["rows"], wl["cols"]
+    src = synth.random_bits((rows, cols), es, synth.BASE_SEED + 7 + 1000 * rank)
+    x = torch.from_numpy(src.view(np.int32)).to(dev)
+    v = desc.desc_view_compile((rows, cols), wl["view"])
+    shape = v.dims[0]
+    y = torch.empty(shape, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    launches = 0
+
+    def step():
+        desc.desc_view_copy(x.data_ptr(), y.data_ptr(), v, "f32", stream.cuda_stream)
+        return desc.desc_last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            launches += step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    ms_max = reduce_scalar(ms, "max", dev)
+    step_bytes = 2 * rows * cols * es
+    value = step_bytes * world * args.steps / (ms_max / 1e3) / 1e9
+    achieved = step_bytes / (ms / args.steps / 1e3) / 1e9
+    peak, peak_src = load_peak()
+    parity = None
+    if rank == 0 and not args.no_oracle:
+        from oracle import views as V
+        exp = V.materialize(src, wl["view"])
+        got = y.cpu().numpy().view(np.uint32)
+        parity = "bit-exact vs oracle (views)" if got.tobytes() == exp.tobytes() else "MISMATCH"
+    if rank == 0:
+        shp, strd, off = v.dims
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"],
+            "data": "synthetic (seeded random bit patterns, host-generated)",
+            "config": {"workload": wl["name"], "rows": rows, "cols": cols,
+                       "view_ops": wl["view"],
+                       "compiled_view": {"shape": shp, "stride": strd, "offset": off},
+                       "parallelism": f"{world} independent replica(s), no collective",
+                       "l2": "inputs larger than L2, no flush",
+                       "timing": "CUDA events around the K launches, max over ranks"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": step_bytes},
+            "parity": parity, "gpu_launches": launches, "cpu_baseline": None, "e2e": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, wl, kernel, world):
     """Same metric end to end through the public host-buffer API desc_transpose_host:
     pinned host input -> (H2D band k+1 | transpose band k | D2H band k-1, pipelined on two
@@ -617,6 +704,8 @@ def main():
     wl = dict(WORKLOADS[args.workload])
     if wl.get("dist") and args.impl == "ours":
         return dist_arm(args, wl, world, rank, local)
+    if wl.get("view") and args.impl == "ours":
+        return view_arm(args, wl, world, rank, local)
     if args.impl == "reference":
         return reference_arm(args, wl, world, rank)
     return ours_arm(args, wl, world, rank, local)

@@ -86,6 +86,7 @@ struct Args {
     int64_t batch, rows, cols, ld_in, ld_out, stride_in, stride_out;
     int es;
     cudaStream_t stream;
+    int rev_rows = 0;   // views only: `in` addresses physical row 0, logical row i = rows-1-i
 };
 
 // ---- device properties (per device, cached) -------------------------------------
@@ -325,6 +326,7 @@ desc_status tma_prepare(Kern kern, int threads, int smem, int tr, int tile_cols,
     p->group = tile_group(*grid, tr, tile_cols, p->tiles_r);
     p->evict_first = dev_knob("DESC_TMA_EVICT", 0);
     p->sched = nullptr;
+    p->rev_rows = a.rev_rows;
     return DESC_OK;
 }
 
@@ -565,6 +567,11 @@ desc_status validate(const Args &a, bool *empty) {
 
 desc_status dispatch(const Args &a, desc_kernel k) {
     const bool tma_ok = tma_eligible(a);
+    if (a.rev_rows) {   // only the TMA-store kernel reads rows mirrored
+        if (!tma_ok || !tma_store_ok(a) || (k != DESC_KERNEL_AUTO && k != DESC_KERNEL_TMA_ST))
+            return fail(DESC_ERR_KERNEL, "reversed rows need the TMA-store kernel");
+        return run_tma2(a);
+    }
     if (k == DESC_KERNEL_TMA && !tma_ok)
         return fail(DESC_ERR_KERNEL, "TMA kernel needs 16-byte aligned bases, ld*size and stride*size");
     if (k == DESC_KERNEL_TMA_ST && !tma_ok)
@@ -899,55 +906,79 @@ desc_status view_copy(const void *in, void *out, const desc_strided_view *view, 
     const int L = nd - 1;
     const char *base = static_cast<const char *>(in) + v.offset * es;
 
-    // transposition of the innermost dim onto an input-contiguous dim: the TMA kernels
-    if (st_in[L] > 1) {
+    // transposition of the innermost dim onto an input-contiguous dim: the TMA kernels.
+    // A negative innermost stride (rows read bottom-up, e.g. rot90 = transpose.map(reverse))
+    // is handled by the TMA-store kernel reading mirrored rows.
+    if (st_in[L] > 1 || st_in[L] < -1) {
         int ec = -1, others = 0, b = -1;
         for (int d = 0; d < L; ++d) {
             if (st_in[d] == 1 && ec < 0) ec = d;
             else { ++others; b = d; }
         }
         if (ec >= 0 && others <= 1 && (b < 0 || st_in[b] > 0)) {
-            Args a{base, out, b < 0 ? 1 : sh[b], sh[L], sh[ec], st_in[L], st_out[ec],
+            const bool rev = st_in[L] < 0;
+            const int64_t ld = rev ? -st_in[L] : st_in[L];
+            const char *phys = rev ? base - (sh[L] - 1) * ld * es : base;
+            Args a{phys, out, b < 0 ? 1 : sh[b], sh[L], sh[ec], ld, st_out[ec],
                    b < 0 ? 0 : st_in[b], b < 0 ? 0 : st_out[b], es, stream};
+            a.rev_rows = rev ? 1 : 0;
             bool empty;
             desc_status s = validate(a, &empty);
-            if (s == DESC_OK) return dispatch(a, DESC_KERNEL_AUTO);
-            if (s != DESC_ERR_SHAPE) return s;
-            // geometry the transpose kernels do not take (e.g. interleaved outputs): gather
+            if (s == DESC_OK) {
+                s = dispatch(a, DESC_KERNEL_AUTO);
+                if (s != DESC_ERR_KERNEL) return s;       // else: not a TMA geometry -> gather
+            } else if (s != DESC_ERR_SHAPE) {
+                return s;
+            }
         }
     }
 
-    desc::ViewRows vr;
-    memset(&vr, 0, sizeof vr);
-    vr.outer_ndim = L;
-    for (int d = 0; d < L; ++d) { vr.outer_shape[d] = sh[d]; vr.outer_stride[d] = st_in[d]; }
-    vr.inner = sh[L];
-    vr.inner_stride = st_in[L];
-    vr.offset = v.offset;
-    vr.rows = total / sh[L];
+    // everything else: outer dims x R2 rows x U cells (view_copy.cuh)
+    desc::ViewTiles vt;
+    memset(&vt, 0, sizeof vt);
+    const int64_t U_el = sh[L], s1 = st_in[L];
+    vt.R2 = L >= 1 ? sh[L - 1] : 1;
+    vt.s2 = L >= 1 ? st_in[L - 1] : 0;
+    vt.outer_ndim = L >= 1 ? L - 1 : 0;
+    vt.outer_count = 1;
+    for (int d = 0; d < vt.outer_ndim; ++d) {
+        vt.outer_shape[d] = sh[d];
+        vt.outer_stride[d] = st_in[d];
+        vt.outer_count *= sh[d];
+    }
+    vt.offset = v.offset;
+    const int V = 16 / es;
+    bool aligned = (i0 % 16 == 0) && (o0 % 16 == 0) && (U_el * es) % 16 == 0 &&
+                   (vt.R2 == 1 || (vt.s2 * es) % 16 == 0);
+    for (int d = 0; d < vt.outer_ndim && aligned; ++d) aligned = (vt.outer_stride[d] * es) % 16 == 0;
+    int mode = 0;
+    if (aligned && s1 == 1 && (v.offset * es) % 16 == 0) mode = 1;
+    else if (aligned && s1 == -1 && ((v.offset - V + 1) * es) % 16 == 0) mode = 2;
+    vt.U = mode ? U_el / V : U_el;
+    vt.s1 = s1;
+    // work items of ~4096 cells (64 KB when vectorised)
+    if (vt.U >= 4096) { vt.uch = 4096; vt.rch = 1; }
+    else { vt.uch = vt.U; vt.rch = (4096 + vt.U - 1) / vt.U; }
+    if (vt.rch > vt.R2) vt.rch = vt.R2;
+    vt.n_uchunks = (vt.U + vt.uch - 1) / vt.uch;
+    vt.n_rchunks = (vt.R2 + vt.rch - 1) / vt.rch;
+    vt.items = vt.outer_count * vt.n_rchunks * vt.n_uchunks;
+    int64_t w = vt.uch < 256 ? vt.uch : 256;
+    vt.ulog = 0;
+    while ((1LL << vt.ulog) < w) ++vt.ulog;
     DevInfo di;
     if (desc_status st = device_info(dev, &di)) return st;
-    const int grid = (int)(vr.rows < (int64_t)di.sms * 16 ? vr.rows : (int64_t)di.sms * 16);
-    bool vec = vr.inner_stride == 1 && (i0 % 16 == 0) && (o0 % 16 == 0) &&
-               (v.offset * es) % 16 == 0 && (vr.inner * es) % 16 == 0;
-    for (int d = 0; d < L && vec; ++d) vec = (vr.outer_stride[d] * es) % 16 == 0;
-    if (vec)
-        desc::view_rows_vec_kernel<<<grid, 256, 0, stream>>>(static_cast<const char *>(in),
-                                                             static_cast<char *>(out), vr, es);
-    else if (es == 8)
-        desc::view_rows_kernel<unsigned long long><<<grid, 256, 0, stream>>>(
-            static_cast<const unsigned long long *>(in), static_cast<unsigned long long *>(out), vr);
-    else if (es == 4)
-        desc::view_rows_kernel<uint32_t><<<grid, 256, 0, stream>>>(
-            static_cast<const uint32_t *>(in), static_cast<uint32_t *>(out), vr);
-    else if (es == 2)
-        desc::view_rows_kernel<uint16_t><<<grid, 256, 0, stream>>>(
-            static_cast<const uint16_t *>(in), static_cast<uint16_t *>(out), vr);
-    else
-        desc::view_rows_kernel<uint8_t><<<grid, 256, 0, stream>>>(
-            static_cast<const uint8_t *>(in), static_cast<uint8_t *>(out), vr);
+    const int grid = (int)(vt.items < (int64_t)di.sms * 8 ? vt.items : (int64_t)di.sms * 8);
+    const char *ci = static_cast<const char *>(in);
+    char *co = static_cast<char *>(out);
+    if (mode == 1) desc::view_tiles_kernel<uint4, 1><<<grid, 256, 0, stream>>>(ci, co, vt, es);
+    else if (mode == 2) desc::view_tiles_kernel<uint4, 2><<<grid, 256, 0, stream>>>(ci, co, vt, es);
+    else if (es == 8) desc::view_tiles_kernel<unsigned long long, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
+    else if (es == 4) desc::view_tiles_kernel<uint32_t, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
+    else if (es == 2) desc::view_tiles_kernel<uint16_t, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
+    else desc::view_tiles_kernel<uint8_t, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
     e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "view_rows_kernel launch");
+    if (e != cudaSuccess) return cuda_fail(e, "view_tiles_kernel launch");
     g_last_launches = 1;
     return DESC_OK;
 }

@@ -156,8 +156,12 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
                 for (int nb = 0; nb < NB; ++nb) {
                     const uint32_t dst = in_base + s * C::STAGE_BYTES + nb * C::BOX_BYTES;
                     const int32_t c0 = tc.tj * C::TILE_COLS + nb * C::TC;
-                    if (p.rank3) ptx::tma_load_3d(dst, &map_in, fb, c0, tc.ti * TR, (int32_t)tc.bt, policy);
-                    else ptx::tma_load_2d(dst, &map_in, fb, c0, tc.ti * TR, policy);
+                    // rev_rows: logical rows [ti*TR, ti*TR+TR) are physical rows
+                    // [rows - (ti+1)*TR, rows - ti*TR): a box that may start above row 0
+                    // (zero-filled, never read back as data)
+                    const int32_t r0 = p.rev_rows ? p.rows - (tc.ti + 1) * TR : tc.ti * TR;
+                    if (p.rank3) ptx::tma_load_3d(dst, &map_in, fb, c0, r0, (int32_t)tc.bt, policy);
+                    else ptx::tma_load_2d(dst, &map_in, fb, c0, r0, policy);
                 }
             }
             if (p.sched) sched_release(p);             // this CTA fetched its last id
@@ -190,7 +194,9 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
             const int row0 = VEC * (task_rgrp(q) * L::A_PER_WARP + a_lane);
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
-                const int row = row0 + k;
+                // logical row row0+k lives in physical box row TR-1-(row0+k) when reversed;
+                // (TR-1-x) & 7 == 7 ^ (x & 7), so the phase stays conflict-free
+                const int row = p.rev_rows ? TR - 1 - (row0 + k) : row0 + k;
                 r[q][k] = ptx::lds128(sbase + task_box(q) * C::BOX_BYTES + row * 128 +
                                       ((task_chunk(q) ^ (row & 7)) << 4));
             }

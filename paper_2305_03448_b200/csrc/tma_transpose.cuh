@@ -41,6 +41,7 @@ struct TmaParams {
     int32_t rank3;       // 1 => 3-D tensor map (batch > 1)
     int32_t group;       // tile rows per raster group (>= 1), see tile_coords
     int32_t evict_first; // 1 => L2 evict_first hint on the TMA loads
+    int32_t rev_rows;    // 1 => logical input row i is physical row rows-1-i (TMA-store kernel)
     int64_t ntiles;
     unsigned long long *sched;  // dynamic tile counter {next, done} (nullptr: static)
 };

@@ -6,27 +6,39 @@
 // analog of "views are compiled into raw indices ... in reversed order", P:509-511,
 // P:1039-1042) and the device materialises it.  The dispatcher (desc_transpose.cu) sends
 // views whose innermost output dim is a transposition onto the TMA transpose kernels; the
-// rest land here: one CTA per output row (the view's innermost dim), 16-byte vectors when
-// every row is contiguous and aligned on both sides, element cells otherwise.
+// rest land here.
+//
+// Work decomposition: after merging, the view is  outer dims x R2 rows x U cells, the cells
+// of a row at input stride s1 (+1, -1 or anything), rows at input stride s2.  A work item is
+// one (outer index, row chunk, cell chunk): the outer mixed-radix decomposition is paid once
+// per item, rows inside the item cost a multiply.  Threads map onto (row, cell) with a
+// power-of-two cell width (shift/mask, no division); the output is contiguous, so a warp
+// always writes consecutive 16-byte units (or cells).  Cells are 16-byte vectors whenever
+// every row is aligned and s1 = +1 (plain) or -1 (vector loaded from the mirrored position
+// and its elements reversed in registers), else single elements.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 namespace desc {
 
 constexpr int kMaxViewDims = 8;
 
-struct ViewRows {
-    int32_t outer_ndim;                  // dims other than the innermost
+struct ViewTiles {
+    int32_t outer_ndim;
     int64_t outer_shape[kMaxViewDims];
-    int64_t outer_stride[kMaxViewDims];  // input element strides of the outer dims
-    int64_t inner;                       // innermost extent (row length, elements)
-    int64_t inner_stride;                // input stride of the innermost dim (elements)
+    int64_t outer_stride[kMaxViewDims];  // input strides of the outer dims (elements)
+    int64_t R2, s2;                      // rows per outer index and their input stride
+    int64_t U;                           // cells per row
+    int64_t s1;                          // input stride between cells (elements; +/-1 for vec)
     int64_t offset;                      // input element offset of view element 0
-    int64_t rows;                        // product of outer_shape
+    int64_t outer_count;                 // product of outer_shape
+    int64_t rch, uch;                    // row / cell chunk of a work item
+    int64_t n_rchunks, n_uchunks, items;
+    int32_t ulog;                        // log2 of the thread cell width (pow2 >= min(uch, 256))
 };
 
-// Input element offset of the first element of output row r (mixed-radix decomposition).
-__device__ __forceinline__ int64_t view_row_offset(const ViewRows &v, int64_t r) {
+__device__ __forceinline__ int64_t outer_offset(const ViewTiles &v, int64_t r) {
     int64_t off = v.offset;
     for (int d = v.outer_ndim - 1; d >= 0; --d) {
         const int64_t n = v.outer_shape[d];
@@ -37,46 +49,80 @@ __device__ __forceinline__ int64_t view_row_offset(const ViewRows &v, int64_t r)
     return off;
 }
 
-// Cell = element-sized word; inner_stride arbitrary (negative after reverse).
-template <typename Cell>
-__global__ void __launch_bounds__(256)
-view_rows_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, const ViewRows v) {
-    for (int64_t r = blockIdx.x; r < v.rows; r += gridDim.x) {
-        const Cell *src = in + view_row_offset(v, r);
-        Cell *dst = out + r * v.inner;
-        int64_t u = threadIdx.x;
-        for (; u + 3 * blockDim.x < v.inner; u += 4 * blockDim.x) {
-            const Cell c0 = src[u * v.inner_stride];
-            const Cell c1 = src[(u + blockDim.x) * v.inner_stride];
-            const Cell c2 = src[(u + 2 * blockDim.x) * v.inner_stride];
-            const Cell c3 = src[(u + 3 * blockDim.x) * v.inner_stride];
-            dst[u] = c0;
-            dst[u + blockDim.x] = c1;
-            dst[u + 2 * blockDim.x] = c2;
-            dst[u + 3 * blockDim.x] = c3;
-        }
-        for (; u < v.inner; u += blockDim.x) dst[u] = src[u * v.inner_stride];
-    }
+__device__ __forceinline__ uint4 reverse_elems(const uint4 &x, int es) {
+    if (es == 8) return make_uint4(x.z, x.w, x.x, x.y);
+    if (es == 4) return make_uint4(x.w, x.z, x.y, x.x);
+    if (es == 2)
+        return make_uint4(__byte_perm(x.w, 0, 0x1032), __byte_perm(x.z, 0, 0x1032),
+                          __byte_perm(x.y, 0, 0x1032), __byte_perm(x.x, 0, 0x1032));
+    return make_uint4(__byte_perm(x.w, 0, 0x0123), __byte_perm(x.z, 0, 0x0123),
+                      __byte_perm(x.y, 0, 0x0123), __byte_perm(x.x, 0, 0x0123));
 }
 
-// Contiguous, 16-byte aligned rows on both sides: inner counted in uint4 units.
-__global__ void __launch_bounds__(256)
-view_rows_vec_kernel(const char *__restrict__ in, char *__restrict__ out, const ViewRows v,
-                     int es) {
-    const int64_t units = v.inner * es / 16;
-    for (int64_t r = blockIdx.x; r < v.rows; r += gridDim.x) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(in + view_row_offset(v, r) * es);
-        uint4 *dst = reinterpret_cast<uint4 *>(out + r * v.inner * es);
-        int64_t u = threadIdx.x;
-        for (; u + 3 * blockDim.x < units; u += 4 * blockDim.x) {
-            const uint4 a = src[u], b = src[u + blockDim.x], c = src[u + 2 * blockDim.x],
-                        d = src[u + 3 * blockDim.x];
-            dst[u] = a;
-            dst[u + blockDim.x] = b;
-            dst[u + 2 * blockDim.x] = c;
-            dst[u + 3 * blockDim.x] = d;
+template <typename Cell, int MODE>
+struct CellIO {
+    using T = typename std::conditional<MODE == 0, Cell, uint4>::type;
+    static constexpr int CB = MODE == 0 ? (int)sizeof(Cell) : 16;     // bytes per cell
+    __device__ static T load(const char *in, int64_t in_row, int64_t u, int64_t s1, int es) {
+        if constexpr (MODE == 0) {
+            return *reinterpret_cast<const Cell *>(in + (in_row + u * s1) * CB);
+        } else if constexpr (MODE == 1) {
+            return *reinterpret_cast<const uint4 *>(in + in_row * es + u * 16);
+        } else {
+            // output cell u holds view elements u*V .. u*V+V-1 = input elements
+            // in_row - u*V - (V-1) .. in_row - u*V, in reverse order
+            const int V = 16 / es;
+            const int64_t first = in_row - u * V - (V - 1);
+            return reverse_elems(*reinterpret_cast<const uint4 *>(in + first * es), es);
         }
-        for (; u < units; u += blockDim.x) dst[u] = src[u];
+    }
+};
+
+// MODE 0: element cells (Cell), any s1.   MODE 1: 16-byte cells, s1 = +1.
+// MODE 2: 16-byte cells, s1 = -1 (mirrored load + in-register element reversal).
+// Short rows: up to 4 rows' loads are in flight per thread before their stores.
+template <typename Cell, int MODE>
+__global__ void __launch_bounds__(256)
+view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const ViewTiles v, int es) {
+    using IO = CellIO<Cell, MODE>;
+    using T = typename IO::T;
+    constexpr int CB = IO::CB;
+    const int uw = 1 << v.ulog;                                    // thread cell width
+    const int rpp = blockDim.x >> v.ulog;                          // rows per pass (>= 1)
+    const int tu = threadIdx.x & (uw - 1);
+    const int tr = threadIdx.x >> v.ulog;
+    for (int64_t w = blockIdx.x; w < v.items; w += gridDim.x) {
+        int64_t q = w;
+        const int64_t uc = q % v.n_uchunks; q /= v.n_uchunks;
+        const int64_t rc = q % v.n_rchunks; q /= v.n_rchunks;
+        const int64_t obase = outer_offset(v, q);                 // elements
+        const int64_t r0 = rc * v.rch, r1 = min(v.R2, r0 + v.rch);
+        const int64_t u0 = uc * v.uch, u1 = min(v.U, u0 + v.uch);
+        char *oitem = out + (q * v.R2) * v.U * CB;                 // output is contiguous
+        if (u1 - u0 <= uw) {                  // one cell per thread per row: unroll rows
+            const int64_t u = u0 + tu;
+            const bool uok = u < u1;
+            for (int64_t r = r0 + tr; r < r1; r += 4 * rpp) {
+                T c[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t rr = r + k * rpp;
+                    if (uok && rr < r1) c[k] = IO::load(in, obase + rr * v.s2, u, v.s1, es);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t rr = r + k * rpp;
+                    if (uok && rr < r1) *reinterpret_cast<T *>(oitem + (rr * v.U + u) * CB) = c[k];
+                }
+            }
+        } else {                              // long rows: consecutive cells per warp
+            for (int64_t r = r0 + tr; r < r1; r += rpp) {
+                const int64_t in_row = obase + r * v.s2;
+                char *orow = oitem + r * v.U * CB;
+                for (int64_t u = u0 + tu; u < u1; u += uw)
+                    *reinterpret_cast<T *>(orow + u * CB) = IO::load(in, in_row, u, v.s1, es);
+            }
+        }
     }
 }
 
