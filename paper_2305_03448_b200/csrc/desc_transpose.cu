@@ -278,15 +278,27 @@ cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t 
                        Args_... args) {
     static const int pdl = dev_knob("DESC_PDL", 1);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3((grid + 1) / 2 * 2);
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    // an explicit cluster launch: st.async (tile ids, TMA-store kernel) is a cluster-scope
+    // op, and compute-sanitizer only accepts it in clusters of >= 2 CTAs (the CTAs of a pair
+    // do not talk to each other; grid is rounded up to even, a spare CTA finds no tile)
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 2;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+    if (pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = n;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -360,7 +372,8 @@ desc_status launch_tma2(const Args &a) {
     // 256 x 1024^2: 332 -> 316 us); with a few tiles per CTA the atomics' latency costs more
     // than the balance gains (2048^2 f64: 14.4 -> 16.4 us), so those stay static.
     static const int dyn = dev_knob("DESC_DYN", 1);
-    if (dyn && p.ntiles >= (int64_t)16 * grid) {
+    static const int dyn_min = dev_knob("DESC_DYN_MIN", 16);   // tiles per CTA (tests: 1)
+    if (dyn && p.ntiles >= (int64_t)dyn_min * grid) {
         int dev = 0;
         cudaGetDevice(&dev);
         // a stream being captured into a CUDA graph cannot allocate: use an existing

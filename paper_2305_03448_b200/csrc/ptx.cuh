@@ -41,6 +41,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "}\n" ::"r"(bar), "r"(parity) : "memory");
 }
 
+// Asynchronous 8-byte store into (this CTA's) shared memory that completes as `bytes` on the
+// mbarrier, like a TMA load: the consumer sees the value after its mbarrier wait.
+__device__ __forceinline__ void st_async_b64(uint32_t addr, uint64_t v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(addr), "l"(v), "r"(bar) : "memory");
+}
+
 // ---- programmatic dependent launch (PDL) ------------------------------------------
 // Block until every prerequisite grid in the stream has completed and its memory is
 // visible (no-op when the kernel was not launched with programmatic serialisation).

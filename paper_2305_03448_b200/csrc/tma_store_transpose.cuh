@@ -104,7 +104,7 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[STAGES];
     __shared__ __align__(8) uint64_t empty_bar[STAGES];
-    __shared__ int64_t tile_id[STAGES];
+    __shared__ __align__(8) int64_t tile_id[STAGES];
 
     const uint32_t in_base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
     const uint32_t out_base = in_base + STAGES * C::STAGE_BYTES;
@@ -131,8 +131,8 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
             const uint64_t policy = p.evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
             // Tile ids: static round robin, or (p.sched != nullptr) fetched from a global
             // counter so that faster SMs take more tiles (dynamic scheduling).  The next id
-            // is fetched one tile ahead to hide the atomic's latency.  The id travels to the
-            // consumers through tile_id[s] (published by the full barrier's release).
+            // is fetched one tile ahead to hide the atomic's latency.  The id reaches the
+            // consumers through tile_id[s], written with st.async completing on full[s].
             auto fetch = [&](int it) -> int64_t {
                 return p.sched ? (int64_t)atomicAdd(p.sched, 1ull)
                                : (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
@@ -144,14 +144,17 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
                 const int64_t t = t_next;
                 if (t < p.ntiles) t_next = fetch(it + 1);
                 ptx::mbar_wait(ptx::smem_u32(&empty_bar[s]), ph ^ 1u);
-                tile_id[s] = t;
+                // the tile id travels like the tile: an async store completing on full[s]
                 const uint32_t fb = ptx::smem_u32(&full_bar[s]);
+                const uint32_t ta = ptx::smem_u32(&tile_id[s]);
                 if (t >= p.ntiles) {                   // no more work: tell the consumers
-                    ptx::mbar_arrive(fb);
+                    ptx::mbar_arrive_expect_tx(fb, 8);
+                    ptx::st_async_b64(ta, (uint64_t)t, fb);
                     break;
                 }
                 const TileCoord tc = tile_coords(t, p);
-                ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+                ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES + 8);
+                ptx::st_async_b64(ta, (uint64_t)t, fb);
 #pragma unroll
                 for (int nb = 0; nb < NB; ++nb) {
                     const uint32_t dst = in_base + s * C::STAGE_BYTES + nb * C::BOX_BYTES;

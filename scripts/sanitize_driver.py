@@ -49,6 +49,32 @@ def main():
             bad += not ok
             print(f"{k:7s} batch={batch} {rows}x{cols} es={es}: {'ok' if ok else 'MISMATCH'}",
                   flush=True)
+    # dynamically scheduled TMA-store launches with stage reuse (run the driver with
+    # DESC_DYN_MIN=1 so that this modest size takes the dynamic path)
+    from oracle import views as V
+    big = synth.random_bits((2048, 2048), 4, 99)
+    xb = torch.from_numpy(big.view(np.int32)).cuda()
+    # outputs are zero-filled first: initcheck does not see TMA bulk-tensor stores as
+    # initialising writes (it would flag every byte the TMA-store kernel produced)
+    yb = desc.transpose(xb, torch.zeros((2048, 2048), dtype=torch.int32, device="cuda"))
+    torch.cuda.synchronize()
+    ok = yb.cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(big).tobytes()
+    bad += not ok
+    print(f"tma_st 2048x2048 es=4 (dynamic when DESC_DYN_MIN=1): {'ok' if ok else 'MISMATCH'}",
+          flush=True)
+    # view copies: every dispatch path
+    small = synth.random_bits((192, 320), 4, 7)
+    xs = torch.from_numpy(small.view(np.int32)).cuda()
+    for ops in ([("transpose", 0, 0), ("reverse", 0, 1)],                     # mirrored TMA
+                [("group", 64, 0), ("group", 64, 2), ("transpose", 0, 1)],   # 16-byte rows
+                [("reverse", 0, 0), ("reverse", 0, 1)],                      # reversed vectors
+                [("split_snd", 7, 1), ("reverse", 0, 0)]):                   # element gather
+        shape = desc.desc_view_compile(tuple(xs.shape), ops, tuple(xs.stride())).dims[0]
+        y = desc.view_copy(xs, ops, out=torch.zeros(shape, dtype=xs.dtype, device="cuda"))
+        torch.cuda.synchronize()
+        ok = y.cpu().numpy().view(np.uint32).tobytes() == V.materialize(small, ops).tobytes()
+        bad += not ok
+        print(f"view {ops}: {'ok' if ok else 'MISMATCH'}", flush=True)
     print("sanitize driver:", "PASS" if bad == 0 else f"{bad} FAILURES")
     return 1 if bad else 0
 
