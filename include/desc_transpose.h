@@ -209,7 +209,7 @@ desc_status desc_view_compile(int32_t ndim, const int64_t *shape, const int64_t 
 desc_status desc_view_copy(const void *in, void *out, const desc_strided_view *view,
                            desc_dtype dtype, void *stream);
 
-/* Recommended workspace bytes for desc_transpose_host (double-buffered 1024-row bands). */
+/* Recommended workspace bytes for desc_transpose_host (double-buffered 512-row bands). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);
 
 /* Number of kernel launches the last successful call of this thread issued (0 for an

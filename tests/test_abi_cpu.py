@@ -121,7 +121,7 @@ def test_host_entry_validation(lib):
     assert _status(f, *args, 1, 8, 8, 8, 8, 0, 0, 42, FAKE_OUT, 4096, None) == 3    # dtype
     assert _status(f, h_in.ctypes.data, h_in.ctypes.data, 1, 8, 8, 8, 8, 0, 0, 0, FAKE_OUT,
                    4096, None) == 4                                                # alias
-    assert desc.desc_transpose_host_workspace(8192, 8192, "f32") == 2 * 2 * 1024 * 8192 * 4
+    assert desc.desc_transpose_host_workspace(8192, 8192, "f32") == 2 * 2 * 512 * 8192 * 4
     assert desc.desc_transpose_host_workspace(0, 8, "f32") == 0
 
 
