@@ -24,16 +24,18 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "transpose_ref.c")
+_SRCS = [_SRC, os.path.join(_HERE, "reduce_scan_ref.c")]
 _LIB = os.path.join(_HERE, "liboracle_transpose.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc -O2 (plain C, no intrinsics, no threads)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(
+            os.path.getmtime(_LIB) < os.path.getmtime(src) for src in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, *_SRCS])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -49,6 +51,13 @@ def _load():
         lib.oracle_transpose.argtypes = [ctypes.c_void_p, ctypes.c_void_p,
                                          i64, i64, i64, i64, i64]
         lib.oracle_transpose.restype = ctypes.c_int
+        vp = ctypes.c_void_p
+        for name in ("oracle_block_reduce_int", "oracle_block_reduce_float"):
+            getattr(lib, name).argtypes = [vp, vp, i64, i64, i64]
+            getattr(lib, name).restype = ctypes.c_int
+        for name in ("oracle_scan_int", "oracle_scan_float"):
+            getattr(lib, name).argtypes = [vp, vp, i64, i64]
+            getattr(lib, name).restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -106,3 +115,42 @@ def time_transpose(in_buf: np.ndarray, out_buf: np.ndarray, batch: int, rows: in
                       stride_in, stride_out, es)
         times.append(time.perf_counter() - t0)
     return times
+
+
+# ---- block-wide reduction and scan ----
+def _is_float(a: np.ndarray) -> bool:
+    return a.dtype.kind == "f"
+
+
+def block_reduce(a: np.ndarray, block: int) -> np.ndarray:
+    """out[b] = sum of a[b*B : (b+1)*B] -- integers wrap (same dtype), floats are
+    sequential fp64 sums (float64 result).  oracle/reduce_scan_ref.c."""
+    a = np.ascontiguousarray(a).reshape(-1)
+    if block <= 0:
+        raise ValueError("oracle: block must be positive")
+    nb = -(-a.size // block)
+    if _is_float(a):
+        out = np.empty(nb, dtype=np.float64)
+        rc = _load().oracle_block_reduce_float(a.ctypes.data, out.ctypes.data, a.size, block,
+                                               a.itemsize)
+    else:
+        out = np.empty(nb, dtype=a.dtype)
+        rc = _load().oracle_block_reduce_int(a.ctypes.data, out.ctypes.data, a.size, block,
+                                             a.itemsize)
+    if rc:
+        raise ValueError("oracle: arguments outside the definition")
+    return out
+
+
+def scan(a: np.ndarray) -> np.ndarray:
+    """Inclusive prefix sum -- integers wrap (same dtype), floats sequential fp64."""
+    a = np.ascontiguousarray(a).reshape(-1)
+    if _is_float(a):
+        out = np.empty(a.size, dtype=np.float64)
+        rc = _load().oracle_scan_float(a.ctypes.data, out.ctypes.data, a.size, a.itemsize)
+    else:
+        out = np.empty(a.size, dtype=a.dtype)
+        rc = _load().oracle_scan_int(a.ctypes.data, out.ctypes.data, a.size, a.itemsize)
+    if rc:
+        raise ValueError("oracle: arguments outside the definition")
+    return out
