@@ -63,6 +63,13 @@ VIEW_WORKLOADS = {
 for _k, (_n, _ops) in VIEW_WORKLOADS.items():
     WORKLOADS[_k] = dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4, view=_ops,
                          name=_n + " (SURVEY 8(f) NEXT #2)")
+WORKLOADS["reduce64M_f32"] = dict(batch=1, rows=1, cols=1 << 26, dtype="f32", es=4, op="reduce",
+                                  block=1024, name="block-wide reduction, n = 2^26 f32 (256 MB), "
+                                  "block 1024 (SURVEY 8(f) NEXT #3, P:1047)")
+WORKLOADS["scan64M_f32"] = dict(batch=1, rows=1, cols=1 << 26, dtype="f32", es=4, op="scan",
+                                name="inclusive scan, n = 2^26 f32 (256 MB) (SURVEY 8(f) NEXT #4, P:1047)")
+WORKLOADS["scan64M_i32"] = dict(batch=1, rows=1, cols=1 << 26, dtype="i32", es=4, op="scan",
+                                name="inclusive scan, n = 2^26 i32 (256 MB) (SURVEY 8(f) NEXT #4, P:1047)")
 NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU
 
 
@@ -640,6 +647,105 @@ def view_arm(args, wl, world, rank, local):
     return 0
 
 
+def op_arm(args, wl, world, rank, local):
+    """the paper's other memory-bound benchmarks -- one
+    step = one desc_block_reduce / desc_scan launch over the whole array; parity vs the
+    oracle (integers bit-exact, floats within the summation-order bound)."""
+    import torch
+    import paper_2305_03448_b200 as desc
+
+    local = local_device(local)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    desc.load()
+    if world > 1:
+        init_pg(dev)
+    n, es, op = wl["cols"], wl["es"], wl["op"]
+    npdt = {"f32": np.float32, "i32": np.int32}[wl["dtype"]]
+    a = (synth.random_floats(n, npdt, synth.BASE_SEED + 11 + rank) if npdt == np.float32
+         else synth.random_ints(n, npdt, synth.BASE_SEED + 11 + rank))
+    x = torch.from_numpy(a).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    if op == "reduce":
+        B = wl["block"]
+        y = torch.empty(-(-n // B), dtype=x.dtype, device=dev)
+        step_bytes = (n + y.numel()) * es
+
+        def step():
+            desc.desc_block_reduce(x.data_ptr(), y.data_ptr(), n, B, wl["dtype"], stream.cuda_stream)
+            return desc.desc_last_launch_count()
+    else:
+        y = torch.empty_like(x)
+        ws = desc.desc_scan_workspace(n, wl["dtype"])
+        work = torch.empty(ws, dtype=torch.uint8, device=dev)
+        step_bytes = 2 * n * es
+
+        def step():
+            desc.desc_scan(x.data_ptr(), y.data_ptr(), n, wl["dtype"], work.data_ptr(), ws,
+                           stream.cuda_stream)
+            return desc.desc_last_launch_count()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    launches = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            launches += step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    ms_max = reduce_scalar(ms, "max", dev)
+    value = step_bytes * world * args.steps / (ms_max / 1e3) / 1e9
+    achieved = step_bytes / (ms / args.steps / 1e3) / 1e9
+    peak, peak_src = load_peak()
+    parity = None
+    if rank == 0 and not args.no_oracle:
+        import oracle
+        got = y.cpu().numpy()
+        if op == "reduce":
+            ref = oracle.block_reduce(a, wl["block"])
+            absx = oracle.block_reduce(np.abs(a).astype(np.float64), wl["block"])
+            m = np.minimum(wl["block"], n - np.arange(ref.size) * wl["block"])
+        else:
+            ref = oracle.scan(a)
+            absx = oracle.scan(np.abs(a).astype(np.float64))
+            m = np.arange(1, n + 1)
+        if npdt == np.float32:
+            tol = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64) + \
+                2.0 * m * 2.0 ** -53 * absx
+            ok = bool(np.all(np.abs(got.astype(np.float64) - ref) <= tol))
+            parity = ("within the fp summation-order bound vs oracle" if ok else "MISMATCH")
+        else:
+            parity = "bit-exact vs oracle" if got.tobytes() == ref.tobytes() else "MISMATCH"
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"],
+            "data": "synthetic (seeded, host-generated)",
+            "config": {"workload": wl["name"], "n": n, "block": wl.get("block"),
+                       "parallelism": f"{world} independent replica(s), no collective",
+                       "l2": "inputs larger than L2, no flush",
+                       "timing": "CUDA events around the K launches, max over ranks"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": peak_src + ("; read-only stream, may exceed a copy's "
+                                                    "read+write rate" if op == "reduce" else ""),
+                         "algorithmic_bytes_per_launch": step_bytes},
+            "parity": parity, "gpu_launches": launches, "cpu_baseline": None, "e2e": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, wl, kernel, world):
     """Same metric end to end through the public host-buffer API desc_transpose_host:
     pinned host input -> (H2D band k+1 | transpose band k | D2H band k-1, pipelined on two
@@ -706,6 +812,8 @@ def main():
         return dist_arm(args, wl, world, rank, local)
     if wl.get("view") and args.impl == "ours":
         return view_arm(args, wl, world, rank, local)
+    if wl.get("op") and args.impl == "ours":
+        return op_arm(args, wl, world, rank, local)
     if args.impl == "reference":
         return reference_arm(args, wl, world, rank)
     return ours_arm(args, wl, world, rank, local)

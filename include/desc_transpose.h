@@ -209,6 +209,25 @@ desc_status desc_view_compile(int32_t ndim, const int64_t *shape, const int64_t 
 desc_status desc_view_copy(const void *in, void *out, const desc_strided_view *view,
                            desc_dtype dtype, void *stream);
 
+/* ---- the paper's other memory-bound benchmarks ----
+ * Block-wide reduction: out[b] = sum(in[b*block .. min(n, (b+1)*block))), b < ceil(n/block),
+ * out has the input's dtype.  Integers (DESC_U8, DESC_I32, DESC_I64) sum modulo 2^bits
+ * (bit-exact); DESC_F32 accumulates in fp64 and rounds once; DESC_F64 in fp64 (float results
+ * depend on the summation order only within the usual gamma_B * sum|x| bound).  DESC_F16 /
+ * DESC_BF16 give DESC_ERR_DTYPE; block <= 0 or n < 0 give DESC_ERR_SHAPE; in/out overlap
+ * gives DESC_ERR_ALIAS.  Asynchronous on `stream`. */
+desc_status desc_block_reduce(const void *in, void *out, int64_t n, int64_t block,
+                              desc_dtype dtype, void *stream);
+
+/* Inclusive scan: out[i] = sum(in[0..i]), same dtypes and arithmetic as desc_block_reduce.
+ * Single pass (decoupled look-back; the paper's version is two kernels).  Needs a
+ * device workspace of desc_scan_workspace(n, dtype) bytes, 256-byte aligned (tile status;
+ * zeroed by the call with cudaMemsetAsync on `stream`), else DESC_ERR_SHAPE.  in == out
+ * (in place) is allowed; partial overlap gives DESC_ERR_ALIAS. */
+size_t desc_scan_workspace(int64_t n, desc_dtype dtype);
+desc_status desc_scan(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
+                      size_t work_bytes, void *stream);
+
 /* Recommended workspace bytes for desc_transpose_host (double-buffered 512-row bands). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);
 

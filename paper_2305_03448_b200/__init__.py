@@ -22,7 +22,8 @@ __all__ = [
     "desc_status_string", "desc_last_error", "desc_dtype_size", "desc_version",
     "desc_last_launch_count", "desc_copy_batched", "desc_transpose_host",
     "desc_ipc_handle", "desc_ipc_open", "desc_ipc_close", "desc_view_compile",
-    "desc_view_copy", "view_copy", "desc_transpose_host_workspace",
+    "desc_view_copy", "view_copy", "desc_block_reduce", "desc_scan", "desc_scan_workspace",
+    "block_reduce", "scan", "desc_transpose_host_workspace",
     "transpose", "transpose_batched", "transpose_host",
 ]
 
@@ -101,6 +102,12 @@ def load():
     lib.desc_view_compile.restype = ci
     lib.desc_view_copy.argtypes = [vp, vp, ctypes.POINTER(StridedView), ci, vp]
     lib.desc_view_copy.restype = ci
+    lib.desc_block_reduce.argtypes = [vp, vp, i64, i64, ci, vp]
+    lib.desc_block_reduce.restype = ci
+    lib.desc_scan_workspace.argtypes = [i64, ci]
+    lib.desc_scan_workspace.restype = ctypes.c_size_t
+    lib.desc_scan.argtypes = [vp, vp, i64, ci, vp, ctypes.c_size_t, vp]
+    lib.desc_scan.restype = ci
     lib.desc_last_launch_count.argtypes = []
     lib.desc_last_launch_count.restype = ci
     lib.desc_status_string.argtypes = [ci]
@@ -192,6 +199,44 @@ def view_copy(x, ops, out=None):
     if tuple(out.shape) != shape or not out.is_contiguous():
         raise ValueError(f"out must be a contiguous tensor of shape {shape}")
     desc_view_copy(x.data_ptr(), out.data_ptr(), v, x.dtype, _stream_of(x))
+    return out
+
+
+def desc_block_reduce(in_ptr, out_ptr, n, block, dtype, stream=0):
+    return _check(load().desc_block_reduce(in_ptr, out_ptr, n, block, _dt(dtype), stream))
+
+
+def desc_scan_workspace(n, dtype) -> int:
+    return load().desc_scan_workspace(n, _dt(dtype))
+
+
+def desc_scan(in_ptr, out_ptr, n, dtype, d_work_ptr, work_bytes, stream=0):
+    return _check(load().desc_scan(in_ptr, out_ptr, n, _dt(dtype), d_work_ptr, work_bytes,
+                                   stream))
+
+
+def block_reduce(x, block: int, out=None):
+    """Per-block sums of a contiguous 1-D CUDA tensor (see desc_block_reduce)."""
+    import torch
+    x = x.reshape(-1)
+    nb = -(-x.numel() // block) if block > 0 else 0
+    if out is None:
+        out = torch.empty(nb, dtype=x.dtype, device=x.device)
+    desc_block_reduce(x.data_ptr(), out.data_ptr(), x.numel(), block, x.dtype, _stream_of(x))
+    return out
+
+
+def scan(x, out=None, work=None):
+    """Inclusive prefix sum of a contiguous 1-D CUDA tensor (see desc_scan)."""
+    import torch
+    x = x.reshape(-1)
+    if out is None:
+        out = torch.empty_like(x)
+    nbytes = desc_scan_workspace(x.numel(), x.dtype)
+    if work is None:
+        work = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=x.device)
+    desc_scan(x.data_ptr(), out.data_ptr(), x.numel(), x.dtype, work.data_ptr(), work.numel(),
+              _stream_of(x))
     return out
 
 

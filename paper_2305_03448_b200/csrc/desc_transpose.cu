@@ -20,6 +20,7 @@
 #include "tma_store_transpose.cuh"
 #include "copy_kernel.cuh"
 #include "view_copy.cuh"
+#include "reduce_scan.cuh"
 
 namespace {
 
@@ -273,6 +274,30 @@ void sched_lookup(int dev, cudaStream_t stream, unsigned long long **out) {
 // Launch with programmatic stream serialisation (PDL) so that back-to-back transposes
 // overlap launch latency and prologue with the previous kernel's tail; the kernels call
 // griddepcontrol.wait before touching global memory, so stream order is preserved.
+template <typename Kern, typename... Args_>
+cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
+                       Args_... args);
+
+// 2-CTA cluster launch WITHOUT programmatic serialisation (kernels that do not call
+// griddepcontrol.wait, e.g. the scan, whose state is zeroed by a memset just before it).
+template <typename Kern, typename... Args_>
+cudaError_t launch_cluster2(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
+                            Args_... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((grid + 1) / 2 * 2);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename Kern, typename... Args_>
 cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
                        Args_... args) {
@@ -996,9 +1021,181 @@ desc_status view_copy(const void *in, void *out, const desc_strided_view *view, 
     return DESC_OK;
 }
 
+// ---- block-wide reduction and scan -------------------------------
+// element size of the reduce/scan dtypes; 0 for the 2-byte float types (not supported)
+int rs_es(desc_dtype t) {
+    switch (t) {
+        case DESC_U8: return 1;
+        case DESC_I32: case DESC_F32: return 4;
+        case DESC_I64: case DESC_F64: return 8;
+        default: return 0;
+    }
+}
+
+template <typename In>
+desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64_t nb, bool vec,
+                          int sms, cudaStream_t stream) {
+    const In *pi = static_cast<const In *>(in);
+    In *po = static_cast<In *>(out);
+    const int64_t cap = (int64_t)sms * 16;
+    if (B <= 64) {
+        const int64_t g = (nb + 255) / 256;
+        desc::block_reduce_kernel<In, In, 1><<<(int)(g < cap ? g : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
+    } else if (B <= 16384) {
+        const int64_t g = (nb + 7) / 8;
+        desc::block_reduce_kernel<In, In, 32><<<(int)(g < cap ? g : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
+    } else {
+        desc::block_reduce_cta_kernel<In, In><<<(int)(nb < cap ? nb : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "block_reduce launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
+desc_status run_reduce(const void *in, void *out, int64_t n, int64_t B, desc_dtype dtype,
+                       cudaStream_t stream) {
+    g_last_launches = 0;
+    const int es = rs_es(dtype);
+    if (es == 0) return fail(DESC_ERR_DTYPE, "block reduction supports u8, i32, i64, f32, f64");
+    if (n < 0 || B <= 0) return fail(DESC_ERR_SHAPE, "need n >= 0 and block > 0");
+    if (n == 0) return DESC_OK;
+    if (!in || !out) return fail(DESC_ERR_NULL, "null pointer");
+    const int64_t nb = (n + B - 1) / B;
+    int64_t bin, bout;
+    if (!mul_ok(n, es, &bin) || !mul_ok(nb, es, &bout)) return fail(DESC_ERR_SHAPE, "extent overflow");
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(in), o0 = reinterpret_cast<uintptr_t>(out);
+    if (i0 < o0 + (uintptr_t)bout && o0 < i0 + (uintptr_t)bin)
+        return fail(DESC_ERR_ALIAS, "in and out overlap (&uniq, P:576-579)");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (desc_status st = check_memspace(in, dev, "in")) return st;
+    if (desc_status st = check_memspace(out, dev, "out")) return st;
+    DevInfo di;
+    if (desc_status st = device_info(dev, &di)) return st;
+    const bool vec = i0 % 16 == 0;
+    switch (dtype) {
+        case DESC_U8: return launch_reduce<uint8_t>(in, out, n, B, nb, vec, di.sms, stream);
+        case DESC_I32: return launch_reduce<uint32_t>(in, out, n, B, nb, vec, di.sms, stream);
+        case DESC_I64: return launch_reduce<uint64_t>(in, out, n, B, nb, vec, di.sms, stream);
+        case DESC_F32: return launch_reduce<float>(in, out, n, B, nb, vec, di.sms, stream);
+        case DESC_F64: return launch_reduce<double>(in, out, n, B, nb, vec, di.sms, stream);
+        default: return fail(DESC_ERR_DTYPE, "unsupported dtype");
+    }
+}
+
+// scan tiles: 256 threads x ITEMS elements: 128 bytes per thread for 4/8-byte cells (32 KB
+// tiles: few tiles keep the look-back chain short), 64 for bytes (register budget)
+int scan_items(int es) { return es == 1 ? 64 : 128 / es; }
+
+int64_t scan_tiles(int64_t n, int es) {
+    const int64_t T = 256 * (int64_t)scan_items(es);
+    return (n + T - 1) / T;
+}
+
+int64_t scan_workspace_bytes(int64_t n, int es) {
+    const int acc = es == 8 || es == 4 ? 8 : 4;   // f32 accumulates in f64; i32/u8 in u32
+    const int64_t t = scan_tiles(n, es);
+    return 256 + round_up(t * 4, 256) + 2 * round_up(t * acc, 256);
+}
+
+template <typename In, int ITEMS>
+desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool vec,
+                        cudaStream_t stream) {
+    using Acc = typename desc::AccOf<In>::T;
+    const int es = (int)sizeof(In);
+    const int64_t t = scan_tiles(n, es);
+    desc::ScanState<Acc> st;
+    st.counter = reinterpret_cast<uint32_t *>(work);
+    st.flags = reinterpret_cast<uint32_t *>(work + 256);
+    char *vals = work + 256 + round_up(t * 4, 256);
+    st.agg = reinterpret_cast<Acc *>(vals);
+    st.incl = reinterpret_cast<Acc *>(vals + round_up(t * (int64_t)sizeof(Acc), 256));
+    st.dbg = 0;
+    if (t > INT32_MAX) return fail(DESC_ERR_SHAPE, "scan too long");
+    const In *pi = static_cast<const In *>(in);
+    In *po = static_cast<In *>(out);
+    cudaError_t e;
+    // short arrays: one launch with decoupled look-back; long ones: reduce-then-scan
+    static const int single_max = dev_knob("DESC_SCAN_SINGLE_MAX_TILES", 256);
+    if (t <= single_max) {
+        e = cudaMemsetAsync(work, 0, 256 + round_up(t * 4, 256), stream);   // counter + flags
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (scan state)");
+        desc::scan_kernel<In, In, ITEMS><<<(int)t, 256, 0, stream>>>(pi, po, n, st, vec);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+        g_last_launches = 1;
+        return DESC_OK;
+    }
+    const int64_t T = 256 * (int64_t)ITEMS;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    DevInfo di;
+    if (desc_status s = device_info(dev, &di)) return s;
+    const int64_t g1 = (t + 7) / 8, cap = (int64_t)di.sms * 16;       // one warp per tile
+    desc::block_reduce_kernel<In, Acc, 32><<<(int)(g1 < cap ? g1 : cap), 256, 0, stream>>>(
+        pi, st.agg, n, T, t, (reinterpret_cast<uintptr_t>(in) & 15) == 0);
+    desc::scan_aggregates_kernel<Acc><<<1, 1024, 0, stream>>>(st.agg, st.incl, t);
+    desc::scan_tiles_kernel<In, ITEMS><<<(int)t, 256, 0, stream>>>(pi, po, n, st.incl, vec);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+    g_last_launches = 3;
+    return DESC_OK;
+}
+
+desc_status run_scan(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
+                     size_t work_bytes, cudaStream_t stream) {
+    g_last_launches = 0;
+    const int es = rs_es(dtype);
+    if (es == 0) return fail(DESC_ERR_DTYPE, "scan supports u8, i32, i64, f32, f64");
+    if (n < 0) return fail(DESC_ERR_SHAPE, "negative n");
+    if (n == 0) return DESC_OK;
+    if (!in || !out || !d_work) return fail(DESC_ERR_NULL, "null pointer");
+    int64_t bytes;
+    if (!mul_ok(n, es, &bytes)) return fail(DESC_ERR_SHAPE, "extent overflow");
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(in), o0 = reinterpret_cast<uintptr_t>(out);
+    if (i0 != o0 && i0 < o0 + (uintptr_t)bytes && o0 < i0 + (uintptr_t)bytes)
+        return fail(DESC_ERR_ALIAS, "in and out partially overlap (in == out is allowed)");
+    if ((int64_t)work_bytes < scan_workspace_bytes(n, es) || (reinterpret_cast<uintptr_t>(d_work) & 255))
+        return fail(DESC_ERR_SHAPE, "d_work must be 256-byte aligned and >= desc_scan_workspace(n)");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (desc_status st = check_memspace(in, dev, "in")) return st;
+    if (desc_status st = check_memspace(out, dev, "out")) return st;
+    if (desc_status st = check_memspace(d_work, dev, "d_work")) return st;
+    const bool vec = i0 % 16 == 0 && o0 % 16 == 0;
+    char *w = static_cast<char *>(d_work);
+    switch (dtype) {
+        case DESC_U8: return launch_scan<uint8_t, 64>(in, out, n, w, vec, stream);
+        case DESC_I32: return launch_scan<uint32_t, 32>(in, out, n, w, vec, stream);
+        case DESC_I64: return launch_scan<uint64_t, 16>(in, out, n, w, vec, stream);
+        case DESC_F32: return launch_scan<float, 32>(in, out, n, w, vec, stream);
+        case DESC_F64: return launch_scan<double, 16>(in, out, n, w, vec, stream);
+        default: return fail(DESC_ERR_DTYPE, "unsupported dtype");
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+desc_status desc_block_reduce(const void *in, void *out, int64_t n, int64_t block,
+                              desc_dtype dtype, void *stream) {
+    return run_reduce(in, out, n, block, dtype, static_cast<cudaStream_t>(stream));
+}
+
+size_t desc_scan_workspace(int64_t n, desc_dtype dtype) {
+    const int es = rs_es(dtype);
+    if (es == 0 || n <= 0) return 0;
+    return (size_t)scan_workspace_bytes(n, es);
+}
+
+desc_status desc_scan(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
+                      size_t work_bytes, void *stream) {
+    return run_scan(in, out, n, dtype, d_work, work_bytes, static_cast<cudaStream_t>(stream));
+}
 
 desc_status desc_view_compile(int32_t ndim, const int64_t *shape, const int64_t *strides,
                               const desc_view_op *ops, int32_t nops, desc_strided_view *out) {

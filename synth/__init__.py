@@ -162,3 +162,18 @@ def hash_expected_np(i, j, global_cols: int, seed: int, es: int) -> np.ndarray:
     if es == 4:
         return (h & np.uint64(0xFFFFFFFF)).astype(np.uint32)
     return h
+
+
+def random_floats(n: int, dtype, seed: int, spread: int = 8) -> np.ndarray:
+    """Finite floats with mixed signs and magnitudes: uniform(-1, 1) * 2^k, k uniform in
+    [-spread, spread] (reduction / scan inputs: NaN/inf would make sums meaningless)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    v = rng.uniform(-1.0, 1.0, size=n) * np.exp2(rng.integers(-spread, spread + 1, size=n))
+    return v.astype(dtype)
+
+
+def random_ints(n: int, dtype, seed: int) -> np.ndarray:
+    """Uniform integers over the whole range of `dtype` (sums wrap around)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    info = np.iinfo(dtype)
+    return rng.integers(info.min, info.max, size=n, dtype=dtype, endpoint=True)

@@ -1,0 +1,104 @@
+"""GPU parity of the block-wide reduction and the single-pass scan (C ABI) against the oracle
+(oracle/reduce_scan_ref.c): integers bit-exact (sums mod 2^bits); floats within the bound the
+arithmetic gives -- |gpu - oracle| <= ulp_out(|oracle|) (f32 output rounding) +
+2 * m * 2^-53 * sum|x| (two fp64 summation orders over m terms)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2305_03448_b200 as desc
+
+pytestmark = pytest.mark.gpu
+
+INTS = (np.uint8, np.int32, np.int64)
+FLOATS = (np.float32, np.float64)
+TORCH = {np.uint8: torch.uint8, np.int32: torch.int32, np.int64: torch.int64,
+         np.float32: torch.float32, np.float64: torch.float64}
+
+
+def _input(n, dt, seed):
+    if dt in INTS:
+        return synth.random_ints(n, dt, seed)
+    return synth.random_floats(n, dt, seed)
+
+
+def _dev(a, offset):
+    """Device copy of `a` starting `offset` elements into a fresh allocation (misalignment)."""
+    t = torch.empty(a.size + offset + 16, dtype=TORCH[a.dtype.type], device="cuda")
+    t[offset:offset + a.size] = torch.from_numpy(a).cuda()
+    return t[offset:offset + a.size]
+
+
+def _ulp(dt, ref):
+    if dt == np.float32:
+        return np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    return np.zeros_like(ref)
+
+
+@pytest.mark.parametrize("dt", INTS + FLOATS)
+@pytest.mark.parametrize("n,B", [(1, 1), (1000, 1), (1000, 3), (12345, 16), (12345, 64),
+                                 (100000, 65), (100000, 1000), (1 << 20, 1024),
+                                 (300000, 16384), (300000, 16385), (1000003, 100000),
+                                 (50, 1000)])
+def test_block_reduce(dt, n, B):
+    for offset in (0, 1):
+        a = _input(n, dt, n + B + offset)
+        x = _dev(a, offset)
+        y = desc.block_reduce(x, B)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy()
+        ref = oracle.block_reduce(a, B)
+        assert got.shape == ref.shape
+        if dt in INTS:
+            assert got.tobytes() == ref.tobytes(), (n, B, offset)
+        else:
+            absx = oracle.block_reduce(np.abs(a).astype(np.float64), B)
+            m = np.minimum(B, n - np.arange(ref.size) * B)
+            tol = _ulp(dt, ref) + 2.0 * m * 2.0 ** -53 * absx
+            assert np.all(np.abs(got.astype(np.float64) - ref) <= tol), (n, B, offset)
+
+
+@pytest.mark.parametrize("dt", INTS + FLOATS)
+@pytest.mark.parametrize("n", [1, 255, 4096, 4097, 100003, (1 << 22) + 3])
+def test_scan(dt, n):
+    for offset in (0, 1):
+        a = _input(n, dt, n + offset)
+        x = _dev(a, offset)
+        y = desc.scan(x)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy()
+        ref = oracle.scan(a)
+        if dt in INTS:
+            assert got.tobytes() == ref.tobytes(), (n, offset)
+        else:
+            absx = oracle.scan(np.abs(a).astype(np.float64))
+            tol = _ulp(dt, ref) + 2.0 * np.arange(1, n + 1) * 2.0 ** -53 * absx
+            assert np.all(np.abs(got.astype(np.float64) - ref) <= tol), (n, offset)
+
+
+def test_scan_in_place_and_repeat():
+    a = synth.random_ints(1 << 20, np.int32, 4)
+    x = torch.from_numpy(a).cuda()
+    work = torch.empty(desc.desc_scan_workspace(a.size, "i32"), dtype=torch.uint8, device="cuda")
+    for _ in range(3):          # workspace reused: the call re-zeroes the tile state
+        y = desc.scan(x, work=work)
+    desc.scan(x, out=x, work=work)     # in place
+    torch.cuda.synchronize()
+    assert x.cpu().numpy().tobytes() == oracle.scan(a).tobytes()
+    assert y.cpu().numpy().tobytes() == oracle.scan(a).tobytes()
+
+
+def test_errors():
+    x = torch.zeros(100, dtype=torch.float16, device="cuda")
+    with pytest.raises(desc.DescError, match="DTYPE"):
+        desc.block_reduce(x, 10)
+    y = torch.zeros(100, dtype=torch.float32, device="cuda")
+    with pytest.raises(desc.DescError, match="SHAPE"):
+        desc.desc_block_reduce(y.data_ptr(), y.data_ptr(), 100, 0, "f32")
+    work = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(desc.DescError, match="SHAPE"):
+        desc.scan(y, work=work)
+    with pytest.raises(desc.DescError, match="ALIAS"):
+        desc.desc_scan(y.data_ptr(), y.data_ptr() + 4, 50, "f32", work.data_ptr(), 1 << 20)
