@@ -75,6 +75,28 @@ def main():
         ok = y.cpu().numpy().view(np.uint32).tobytes() == V.materialize(small, ops).tobytes()
         bad += not ok
         print(f"view {ops}: {'ok' if ok else 'MISMATCH'}", flush=True)
+    # block reduction (thread / warp / CTA groups) and scan (single pass and, with
+    # DESC_SCAN_SINGLE_MAX_TILES=2 in the environment, the three-launch route)
+    for dt, n in ((np.int32, 100003), (np.float32, 70001), (np.int64, 50000), (np.uint8, 90000)):
+        a = (synth.random_ints(n, dt, 5) if dt != np.float32 else synth.random_floats(n, dt, 5))
+        x = torch.from_numpy(a).cuda()
+        for B in (16, 1000, 20000):
+            y = desc.block_reduce(x, B)
+            torch.cuda.synchronize()
+            ref = oracle.block_reduce(a, B)
+            if dt == np.float32:
+                ok = np.allclose(y.cpu().numpy(), ref, rtol=1e-6, atol=1e-6)
+            else:
+                ok = y.cpu().numpy().tobytes() == ref.tobytes()
+            bad += not ok
+            print(f"block_reduce {dt.__name__} n={n} B={B}: {'ok' if ok else 'MISMATCH'}", flush=True)
+        y = desc.scan(x, out=torch.zeros_like(x))
+        torch.cuda.synchronize()
+        ref = oracle.scan(a)
+        ok = (np.allclose(y.cpu().numpy(), ref, rtol=1e-5, atol=1e-3) if dt == np.float32
+              else y.cpu().numpy().tobytes() == ref.tobytes())
+        bad += not ok
+        print(f"scan {dt.__name__} n={n}: {'ok' if ok else 'MISMATCH'}", flush=True)
     print("sanitize driver:", "PASS" if bad == 0 else f"{bad} FAILURES")
     return 1 if bad else 0
 
