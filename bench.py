@@ -46,6 +46,10 @@ WORKLOADS = {
                     name="2048x2048 f64 transpose (BASELINE.json configs[1], the paper's listing shape)"),
     "3000x5000f64": dict(batch=1, rows=3000, cols=5000, dtype="f64", es=8,
                          name="3000x5000 f64 non-tile-multiple transpose (BASELINE.json configs[2])"),
+    "4096f64": dict(batch=1, rows=4096, cols=4096, dtype="f64", es=8,
+                    name="4096x4096 f64 transpose (paper-size extra: 256 MB in+out, P:1051)"),
+    "8192f64": dict(batch=1, rows=8192, cols=8192, dtype="f64", es=8,
+                    name="8192x8192 f64 transpose (paper-size extra: 1 GiB in+out, P:1051)"),
     "batched": dict(batch=256, rows=1024, cols=1024, dtype="f32", es=4, shard=True,
                     name="batched 256x(1024x1024) f32, batch sharded over ranks (BASELINE.json configs[3])"),
     "dist65536": dict(batch=1, rows=65536, cols=65536, dtype="f32", es=4, dist=True,

@@ -1037,12 +1037,14 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
                           int sms, cudaStream_t stream) {
     const In *pi = static_cast<const In *>(in);
     In *po = static_cast<In *>(out);
+    // grid: up to 16 x 256-thread CTAs per SM, grid-striding over the blocks (measured best
+    // against balanced-round and one-block-per-group grids: 0.855 vs 0.834 / 0.833)
     const int64_t cap = (int64_t)sms * 16;
     if (B <= 64) {
-        const int64_t g = (nb + 255) / 256;
+        const int64_t g = (nb + 255) / 256;                            // thread per block
         desc::block_reduce_kernel<In, In, 1><<<(int)(g < cap ? g : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
     } else if (B <= 16384) {
-        const int64_t g = (nb + 7) / 8;
+        const int64_t g = (nb + 7) / 8;                                // warp per block
         desc::block_reduce_kernel<In, In, 32><<<(int)(g < cap ? g : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
     } else {
         desc::block_reduce_cta_kernel<In, In><<<(int)(nb < cap ? nb : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
@@ -1112,7 +1114,6 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     char *vals = work + 256 + round_up(t * 4, 256);
     st.agg = reinterpret_cast<Acc *>(vals);
     st.incl = reinterpret_cast<Acc *>(vals + round_up(t * (int64_t)sizeof(Acc), 256));
-    st.dbg = 0;
     if (t > INT32_MAX) return fail(DESC_ERR_SHAPE, "scan too long");
     const In *pi = static_cast<const In *>(in);
     In *po = static_cast<In *>(out);

@@ -150,8 +150,7 @@ struct ScanState {
     uint32_t *counter;   // tile claim counter
     uint32_t *flags;     // 0 = not ready, 1 = aggregate, 2 = inclusive prefix
     Acc *agg;            // per-tile aggregate
-    Acc *incl;           // per-tile inclusive prefix
-    int dbg;             // development A/B only: 1 = skip the look-back (wrong results)
+    Acc *incl;           // per-tile inclusive prefix (single pass) / exclusive (three-launch)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
@@ -300,7 +299,7 @@ scan_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
                 st.agg[tile] = agg;
                 st_release(&st.flags[tile], 1u);
             }
-            if (!st.dbg) prefix = look_back<Acc, 16>(st, tile, lane);
+            prefix = look_back<Acc, 16>(st, tile, lane);
             if (lane == 0) {
                 st.incl[tile] = prefix + agg;
                 st_release(&st.flags[tile], 2u);
