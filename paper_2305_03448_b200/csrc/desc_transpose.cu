@@ -739,9 +739,32 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
             return cuda_fail(e, "cudaStreamWaitEvent");
     int launches = 0;
     int64_t k = 0;
+    // Band sizes ramp up (band/8, band/4, band/2, band, ...) at the start of the whole call
+    // and down again at its end: the first H2D and the last D2H are the only copies that
+    // cannot overlap the other direction, so making them small shrinks fill and drain.
+    const int64_t total_rows = batch * rows;
+    int64_t done_rows = 0;
+    auto band_at = [&](int64_t r0) {
+        int64_t nb = band;
+        for (int64_t d = 8; d >= 2; d /= 2) {
+            const int64_t small = band / d;
+            if (small < 16) continue;
+            if (done_rows < small * (8 / d)) { nb = small; break; }      // ramp up
+        }
+        const int64_t left = total_rows - done_rows;
+        if (left < 2 * band) {                                            // ramp down
+            const int64_t floor_rows = band / 8 > 16 ? band / 8 : 16;
+            const int64_t half = (left + 1) / 2;
+            nb = nb < half ? nb : half;
+            if (nb < floor_rows) nb = floor_rows < left ? floor_rows : left;
+        }
+        if (nb < 1) nb = 1;
+        return nb < rows - r0 ? nb : rows - r0;
+    };
     for (int64_t b = 0; b < batch; ++b) {
-        for (int64_t r0 = 0; r0 < rows; r0 += band, ++k) {
-            const int64_t nr = rows - r0 < band ? rows - r0 : band;
+        for (int64_t r0 = 0, nr = 0; r0 < rows; r0 += nr, ++k) {
+            nr = band_at(r0);
+            done_rows += nr;
             const int buf = (int)(k & 1);
             cudaStream_t s = hp->s[buf];
             const int64_t ldo_d = round_up(nr, v);
