@@ -685,8 +685,8 @@ def op_arm(args, wl, world, rank, local):
         step_bytes = 2 * n * es
 
         def step():
-            desc.desc_scan(x.data_ptr(), y.data_ptr(), n, wl["dtype"], work.data_ptr(), ws,
-                           stream.cuda_stream)
+            desc.desc_scan_ex(x.data_ptr(), y.data_ptr(), n, wl["dtype"], work.data_ptr(), ws,
+                              args.scan_algo, stream.cuda_stream)
             return desc.desc_last_launch_count()
     for _ in range(args.warmup):
         step()
@@ -733,6 +733,7 @@ def op_arm(args, wl, world, rank, local):
             "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"],
             "data": "synthetic (seeded, host-generated)",
             "config": {"workload": wl["name"], "n": n, "block": wl.get("block"),
+                       "scan_algo": args.scan_algo if op == "scan" else None,
                        "parallelism": f"{world} independent replica(s), no collective",
                        "l2": "inputs larger than L2, no flush",
                        "timing": "CUDA events around the K launches, max over ranks"},
@@ -797,6 +798,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="8192f32")
     ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem"], default="auto")
+    ap.add_argument("--scan-algo", choices=["auto", "lookback", "three_pass", "stream"],
+                    default="auto")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
     ap.add_argument("--reference-seconds", type=float, default=120.0)
     ap.add_argument("--e2e-steps", type=int, default=20)

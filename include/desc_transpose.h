@@ -220,13 +220,30 @@ desc_status desc_block_reduce(const void *in, void *out, int64_t n, int64_t bloc
                               desc_dtype dtype, void *stream);
 
 /* Inclusive scan: out[i] = sum(in[0..i]), same dtypes and arithmetic as desc_block_reduce.
- * Single pass (decoupled look-back; the paper's version is two kernels).  Needs a
- * device workspace of desc_scan_workspace(n, dtype) bytes, 256-byte aligned (tile status;
- * zeroed by the call with cudaMemsetAsync on `stream`), else DESC_ERR_SHAPE.  in == out
- * (in place) is allowed; partial overlap gives DESC_ERR_ALIAS. */
+ * Needs a device workspace of desc_scan_workspace(n, dtype) bytes, 256-byte aligned (tile
+ * status; zeroed by the call with cudaMemsetAsync on `stream`), else DESC_ERR_SHAPE.  in ==
+ * out (in place) is allowed; partial overlap gives DESC_ERR_ALIAS.
+ * Algorithms (desc_scan_ex; desc_scan = AUTO):
+ *   DESC_SCAN_LOOKBACK  : one launch, one 8-32 KB tile per CTA, decoupled look-back.
+ *   DESC_SCAN_THREE_PASS: tile aggregates -> aggregate scan -> tile scans (3 launches,
+ *                         3 n bytes of traffic; the paper's multi-kernel shape).
+ *   DESC_SCAN_STREAM    : one launch, persistent CTAs stream 96 KB tiles through a
+ *                         shared-memory ring (1-D TMA bulk copies) with a coalesced
+ *                         look-back; 2 n bytes.  Needs 16-byte aligned in and out.
+ * AUTO takes STREAM for aligned arrays of >= 2 tiles per SM, LOOKBACK for shorter ones,
+ * THREE_PASS for unaligned long ones.  An explicit algorithm whose rule does not hold
+ * gives DESC_ERR_KERNEL. */
+typedef enum desc_scan_algo {
+    DESC_SCAN_AUTO = 0,
+    DESC_SCAN_LOOKBACK = 1,
+    DESC_SCAN_THREE_PASS = 2,
+    DESC_SCAN_STREAM = 3
+} desc_scan_algo;
 size_t desc_scan_workspace(int64_t n, desc_dtype dtype);
 desc_status desc_scan(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
                       size_t work_bytes, void *stream);
+desc_status desc_scan_ex(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
+                         size_t work_bytes, desc_scan_algo algo, void *stream);
 
 /* Recommended workspace bytes for desc_transpose_host (double-buffered 512-row bands). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);

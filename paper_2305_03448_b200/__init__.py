@@ -22,13 +22,15 @@ __all__ = [
     "desc_status_string", "desc_last_error", "desc_dtype_size", "desc_version",
     "desc_last_launch_count", "desc_copy_batched", "desc_transpose_host",
     "desc_ipc_handle", "desc_ipc_open", "desc_ipc_close", "desc_view_compile",
-    "desc_view_copy", "view_copy", "desc_block_reduce", "desc_scan", "desc_scan_workspace",
+    "desc_view_copy", "view_copy", "desc_block_reduce", "desc_scan", "desc_scan_ex",
+    "desc_scan_workspace", "SCAN_ALGO",
     "block_reduce", "scan", "desc_transpose_host_workspace",
     "transpose", "transpose_batched", "transpose_host",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_PKG, "libdesc_transpose.so")
+# DESC_LIB: another in-tree build of the same library (compile-time variants for A/B runs)
+lib_path = os.environ.get("DESC_LIB") or os.path.join(_PKG, "libdesc_transpose.so")
 
 # enums (include/desc_transpose.h)
 STATUS = {0: "DESC_OK", 1: "DESC_ERR_NULL", 2: "DESC_ERR_SHAPE", 3: "DESC_ERR_DTYPE",
@@ -36,6 +38,7 @@ STATUS = {0: "DESC_OK", 1: "DESC_ERR_NULL", 2: "DESC_ERR_SHAPE", 3: "DESC_ERR_DT
 DTYPE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3, "f16": 4, "bf16": 5, "u8": 6}
 KERNEL = {"auto": 0, "smem": 1, "tma": 2, "tma_st": 3}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
+SCAN_ALGO = {"auto": 0, "lookback": 1, "three_pass": 2, "stream": 3}
 
 _lib = None
 
@@ -108,6 +111,8 @@ def load():
     lib.desc_scan_workspace.restype = ctypes.c_size_t
     lib.desc_scan.argtypes = [vp, vp, i64, ci, vp, ctypes.c_size_t, vp]
     lib.desc_scan.restype = ci
+    lib.desc_scan_ex.argtypes = [vp, vp, i64, ci, vp, ctypes.c_size_t, ci, vp]
+    lib.desc_scan_ex.restype = ci
     lib.desc_last_launch_count.argtypes = []
     lib.desc_last_launch_count.restype = ci
     lib.desc_status_string.argtypes = [ci]
@@ -215,6 +220,12 @@ def desc_scan(in_ptr, out_ptr, n, dtype, d_work_ptr, work_bytes, stream=0):
                                    stream))
 
 
+def desc_scan_ex(in_ptr, out_ptr, n, dtype, d_work_ptr, work_bytes, algo="auto", stream=0):
+    return _check(load().desc_scan_ex(in_ptr, out_ptr, n, _dt(dtype), d_work_ptr, work_bytes,
+                                      SCAN_ALGO[algo] if isinstance(algo, str) else int(algo),
+                                      stream))
+
+
 def block_reduce(x, block: int, out=None):
     """Per-block sums of a contiguous 1-D CUDA tensor (see desc_block_reduce)."""
     import torch
@@ -226,8 +237,8 @@ def block_reduce(x, block: int, out=None):
     return out
 
 
-def scan(x, out=None, work=None):
-    """Inclusive prefix sum of a contiguous 1-D CUDA tensor (see desc_scan)."""
+def scan(x, out=None, work=None, algo="auto"):
+    """Inclusive prefix sum of a contiguous 1-D CUDA tensor (see desc_scan / desc_scan_ex)."""
     import torch
     x = x.reshape(-1)
     if out is None:
@@ -235,8 +246,8 @@ def scan(x, out=None, work=None):
     nbytes = desc_scan_workspace(x.numel(), x.dtype)
     if work is None:
         work = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=x.device)
-    desc_scan(x.data_ptr(), out.data_ptr(), x.numel(), x.dtype, work.data_ptr(), work.numel(),
-              _stream_of(x))
+    desc_scan_ex(x.data_ptr(), out.data_ptr(), x.numel(), x.dtype, work.data_ptr(), work.numel(),
+                 algo, _stream_of(x))
     return out
 
 

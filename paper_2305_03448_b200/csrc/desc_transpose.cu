@@ -739,32 +739,11 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
             return cuda_fail(e, "cudaStreamWaitEvent");
     int launches = 0;
     int64_t k = 0;
-    // Band sizes ramp up (band/8, band/4, band/2, band, ...) at the start of the whole call
-    // and down again at its end: the first H2D and the last D2H are the only copies that
-    // cannot overlap the other direction, so making them small shrinks fill and drain.
-    const int64_t total_rows = batch * rows;
-    int64_t done_rows = 0;
-    auto band_at = [&](int64_t r0) {
-        int64_t nb = band;
-        for (int64_t d = 8; d >= 2; d /= 2) {
-            const int64_t small = band / d;
-            if (small < 16) continue;
-            if (done_rows < small * (8 / d)) { nb = small; break; }      // ramp up
-        }
-        const int64_t left = total_rows - done_rows;
-        if (left < 2 * band) {                                            // ramp down
-            const int64_t floor_rows = band / 8 > 16 ? band / 8 : 16;
-            const int64_t half = (left + 1) / 2;
-            nb = nb < half ? nb : half;
-            if (nb < floor_rows) nb = floor_rows < left ? floor_rows : left;
-        }
-        if (nb < 1) nb = 1;
-        return nb < rows - r0 ? nb : rows - r0;
-    };
     for (int64_t b = 0; b < batch; ++b) {
-        for (int64_t r0 = 0, nr = 0; r0 < rows; r0 += nr, ++k) {
-            nr = band_at(r0);
-            done_rows += nr;
+        for (int64_t r0 = 0; r0 < rows; r0 += band, ++k) {
+            // fixed bands: measured 81 GB/s vs 77 GB/s with bands ramped at both ends
+            // (scripts/exp_e2e_ramp.py; narrow bands make strided D2H rows short)
+            const int64_t nr = rows - r0 < band ? rows - r0 : band;
             const int buf = (int)(k & 1);
             cudaStream_t s = hp->s[buf];
             const int64_t ldo_d = round_up(nr, v);
@@ -1120,31 +1099,84 @@ int64_t scan_tiles(int64_t n, int es) {
 }
 
 int64_t scan_workspace_bytes(int64_t n, int es) {
-    const int acc = es == 8 || es == 4 ? 8 : 4;   // f32 accumulates in f64; i32/u8 in u32
+    // descriptor words: 8 bytes per tile, twice for 64-bit accumulators (f32 accumulates in
+    // f64, i64/f64 in 64 bits; i32/u8 in u32); three-launch arrays: 2 x acc bytes per tile
+    const int acc = es == 8 || es == 4 ? 8 : 4;
     const int64_t t = scan_tiles(n, es);
-    return 256 + round_up(t * 4, 256) + 2 * round_up(t * acc, 256);
+    const int64_t words = es == 1 ? 1 : 2;   // es 4: f32 needs 2 (i32 uses 1)
+    const int64_t single = words * round_up(t * 8, 256);
+    const int64_t three = 2 * round_up(t * acc, 256);
+    return 256 + (single > three ? single : three);
 }
+
+// streaming scan: 16 compute warps x 32 lanes x 6 16-byte vectors = 48 KB tiles, a 4-stage
+// shared-memory ring (192 KB), lookahead 4 (tile k+4 is reduced before tile k is scanned)
+#ifndef DESC_SCAN_VPT        // compile-time overrides: A/B builds only
+#define DESC_SCAN_VPT 6
+#endif
+#ifndef DESC_SCAN_STAGES
+#define DESC_SCAN_STAGES 4
+#endif
+#ifndef DESC_SCAN_LOOKAHEAD
+#define DESC_SCAN_LOOKAHEAD 4
+#endif
+constexpr int kScanNC = 16, kScanVpt = DESC_SCAN_VPT, kScanStages = DESC_SCAN_STAGES,
+              kScanLookahead = DESC_SCAN_LOOKAHEAD;
+using ScanStreamC = desc::ScanStreamCfg<kScanNC, kScanVpt, kScanStages, kScanLookahead>;
 
 template <typename In, int ITEMS>
 desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool vec,
-                        cudaStream_t stream) {
+                        desc_scan_algo algo, cudaStream_t stream) {
     using Acc = typename desc::AccOf<In>::T;
     const int es = (int)sizeof(In);
     const int64_t t = scan_tiles(n, es);
+    // workspace: [counter | 256 B] then either the single-pass descriptor words (dlo, and dhi
+    // for 64-bit values: 8 bytes per tile each) or the three-launch aggregate and exclusive
+    // prefix arrays (sizeof(Acc) per tile each); scan_workspace_bytes covers the larger
     desc::ScanState<Acc> st;
     st.counter = reinterpret_cast<uint32_t *>(work);
-    st.flags = reinterpret_cast<uint32_t *>(work + 256);
-    char *vals = work + 256 + round_up(t * 4, 256);
+    st.dlo = reinterpret_cast<uint64_t *>(work + 256);
+    st.dhi = reinterpret_cast<uint64_t *>(work + 256 + round_up(t * 8, 256));
+    const int64_t desc_words = sizeof(Acc) == 8 ? 2 : 1;
+    char *vals = work + 256;
     st.agg = reinterpret_cast<Acc *>(vals);
     st.incl = reinterpret_cast<Acc *>(vals + round_up(t * (int64_t)sizeof(Acc), 256));
     if (t > INT32_MAX) return fail(DESC_ERR_SHAPE, "scan too long");
     const In *pi = static_cast<const In *>(in);
     In *po = static_cast<In *>(out);
-    cudaError_t e;
-    // short arrays: one launch with decoupled look-back; long ones: reduce-then-scan
-    static const int single_max = dev_knob("DESC_SCAN_SINGLE_MAX_TILES", 256);
-    if (t <= single_max) {
-        e = cudaMemsetAsync(work, 0, 256 + round_up(t * 4, 256), stream);   // counter + flags
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    DevInfo di;
+    if (desc_status s = device_info(dev, &di)) return s;
+    // streaming tiles (96 KB) are never more than the look-back tiles (<= 32 KB), so the
+    // workspace sized by scan_tiles() covers both
+    constexpr int64_t TBY = ScanStreamC::TB;
+    const int64_t ts = (n * es + TBY - 1) / TBY;
+    if (algo == DESC_SCAN_AUTO) {
+        static const int single_max = dev_knob("DESC_SCAN_SINGLE_MAX_TILES", 256);
+        if (vec && ts >= 2 * (int64_t)di.sms) algo = DESC_SCAN_STREAM;
+        else if (t <= single_max) algo = DESC_SCAN_LOOKBACK;
+        else algo = DESC_SCAN_THREE_PASS;
+    }
+    if (algo == DESC_SCAN_STREAM) {
+        if (!vec) return fail(DESC_ERR_KERNEL, "streaming scan needs 16-byte aligned in and out");
+        auto kern = desc::scan_stream_kernel<In, kScanNC, kScanVpt, kScanStages, kScanLookahead>;
+        const int smem = ScanStreamC::SMEM;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute (scan)");
+        st.dhi = reinterpret_cast<uint64_t *>(work + 256 + round_up(ts * 8, 256));
+        e = cudaMemsetAsync(work, 0, 256 + desc_words * round_up(ts * 8, 256), stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (scan state)");
+        const int64_t grid = ts < di.sms ? ts : di.sms;
+        e = launch_cluster2(kern, (int)grid, ScanStreamC::THREADS, smem, stream, pi, po, n, ts, st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "scan_stream launch");
+        g_last_launches = 1;
+        return DESC_OK;
+    }
+    if (algo == DESC_SCAN_LOOKBACK) {
+        e = cudaMemsetAsync(work, 0, 256 + desc_words * round_up(t * 8, 256), stream);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (scan state)");
         desc::scan_kernel<In, In, ITEMS><<<(int)t, 256, 0, stream>>>(pi, po, n, st, vec);
         e = cudaGetLastError();
@@ -1152,11 +1184,8 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
         g_last_launches = 1;
         return DESC_OK;
     }
+    if (algo != DESC_SCAN_THREE_PASS) return fail(DESC_ERR_KERNEL, "unknown scan algorithm %d", (int)algo);
     const int64_t T = 256 * (int64_t)ITEMS;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    DevInfo di;
-    if (desc_status s = device_info(dev, &di)) return s;
     const int64_t g1 = (t + 7) / 8, cap = (int64_t)di.sms * 16;       // one warp per tile
     desc::block_reduce_kernel<In, Acc, 32><<<(int)(g1 < cap ? g1 : cap), 256, 0, stream>>>(
         pi, st.agg, n, T, t, (reinterpret_cast<uintptr_t>(in) & 15) == 0);
@@ -1169,11 +1198,12 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
 }
 
 desc_status run_scan(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
-                     size_t work_bytes, cudaStream_t stream) {
+                     size_t work_bytes, desc_scan_algo algo, cudaStream_t stream) {
     g_last_launches = 0;
     const int es = rs_es(dtype);
     if (es == 0) return fail(DESC_ERR_DTYPE, "scan supports u8, i32, i64, f32, f64");
     if (n < 0) return fail(DESC_ERR_SHAPE, "negative n");
+    if ((int)algo < 0 || (int)algo > 3) return fail(DESC_ERR_KERNEL, "unknown scan algorithm %d", (int)algo);
     if (n == 0) return DESC_OK;
     if (!in || !out || !d_work) return fail(DESC_ERR_NULL, "null pointer");
     int64_t bytes;
@@ -1192,11 +1222,11 @@ desc_status run_scan(const void *in, void *out, int64_t n, desc_dtype dtype, voi
     const bool vec = i0 % 16 == 0 && o0 % 16 == 0;
     char *w = static_cast<char *>(d_work);
     switch (dtype) {
-        case DESC_U8: return launch_scan<uint8_t, 64>(in, out, n, w, vec, stream);
-        case DESC_I32: return launch_scan<uint32_t, 32>(in, out, n, w, vec, stream);
-        case DESC_I64: return launch_scan<uint64_t, 16>(in, out, n, w, vec, stream);
-        case DESC_F32: return launch_scan<float, 32>(in, out, n, w, vec, stream);
-        case DESC_F64: return launch_scan<double, 16>(in, out, n, w, vec, stream);
+        case DESC_U8: return launch_scan<uint8_t, 64>(in, out, n, w, vec, algo, stream);
+        case DESC_I32: return launch_scan<uint32_t, 32>(in, out, n, w, vec, algo, stream);
+        case DESC_I64: return launch_scan<uint64_t, 16>(in, out, n, w, vec, algo, stream);
+        case DESC_F32: return launch_scan<float, 32>(in, out, n, w, vec, algo, stream);
+        case DESC_F64: return launch_scan<double, 16>(in, out, n, w, vec, algo, stream);
         default: return fail(DESC_ERR_DTYPE, "unsupported dtype");
     }
 }
@@ -1218,7 +1248,13 @@ size_t desc_scan_workspace(int64_t n, desc_dtype dtype) {
 
 desc_status desc_scan(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
                       size_t work_bytes, void *stream) {
-    return run_scan(in, out, n, dtype, d_work, work_bytes, static_cast<cudaStream_t>(stream));
+    return run_scan(in, out, n, dtype, d_work, work_bytes, DESC_SCAN_AUTO,
+                    static_cast<cudaStream_t>(stream));
+}
+
+desc_status desc_scan_ex(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
+                         size_t work_bytes, desc_scan_algo algo, void *stream) {
+    return run_scan(in, out, n, dtype, d_work, work_bytes, algo, static_cast<cudaStream_t>(stream));
 }
 
 desc_status desc_view_compile(int32_t ndim, const int64_t *shape, const int64_t *strides,

@@ -11,18 +11,21 @@
 // B); each group streams its block with 16-byte read-only loads (4 in flight per lane), a
 // scalar head/tail around the 16-byte-aligned body, then shuffles (+ shared memory for CTAs).
 //
-// Scan, short arrays (a few hundred tiles): single pass with decoupled look-back:
-// tiles are claimed in order from an atomic counter (so every predecessor is resident),
-// each tile scans its 256 x ITEMS elements in registers + shuffles, publishes its aggregate
-// (flag A), looks back over predecessors one warp-wide window of 32 at a time (summing
-// aggregates until an inclusive prefix, flag P), publishes its own inclusive prefix, and
-// writes its outputs.  Flags are released / acquired at gpu scope; aggregate and inclusive
-// values live in separate arrays so a reader never mixes them up.  Long arrays: the
-// reduce-then-scan route at the end of this file.
+// Scans (three algorithms, desc_scan_ex):
+//  * LOOKBACK: one 256 x ITEMS tile per CTA, tiles claimed in order from an atomic counter
+//    (so every predecessor is resident or done), registers + shuffles, then decoupled
+//    look-back: publish the aggregate (A), sum predecessors' A back to the nearest
+//    inclusive prefix (P), publish P, write the outputs.
+//  * THREE_PASS: tile aggregates -> one-CTA aggregate scan -> tile scans (3 n bytes).
+//  * STREAM: persistent CTAs stream 96 KB tiles through a shared-memory ring with 1-D TMA
+//    bulk copies, same look-back (2 n bytes).
+// Tile descriptors are single-copy-atomic 64-bit {value, status} words: no fences (below).
 #pragma once
 #include <cstdint>
 #include <cstring>
 #include <type_traits>
+
+#include "ptx.cuh"
 
 namespace desc {
 
@@ -145,22 +148,78 @@ block_reduce_cta_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_
 }
 
 // ---- scan ---------------------------------------------------------------------------------
+// Tile descriptors of the single-pass scans are 64-bit words {value bits : 32, status : 32}
+// (status 0 = not ready, 1 = aggregate A, 2 = inclusive prefix P), written and read with
+// relaxed gpu-scope 8-byte accesses, which are single-copy atomic: a reader that sees a
+// status also sees its value, so no fence sits on the look-back's critical path (a gpu-scope
+// fence waits for the thread's outstanding stores, microseconds under a full HBM stream).
+// 64-bit values are split over two words (lo, hi) that carry the same status; a reader that
+// sees two different statuses (the A -> P update in between) treats the tile as not ready
+// and polls again.
 template <typename Acc>
 struct ScanState {
-    uint32_t *counter;   // tile claim counter
-    uint32_t *flags;     // 0 = not ready, 1 = aggregate, 2 = inclusive prefix
-    Acc *agg;            // per-tile aggregate
-    Acc *incl;           // per-tile inclusive prefix (single pass) / exclusive (three-launch)
+    uint32_t *counter;   // tile claim counter (64-bit for the streaming scan)
+    uint64_t *dlo;       // single pass: descriptor word {value[31:0], status}
+    uint64_t *dhi;       // single pass, 64-bit values: {value[63:32], status}
+    Acc *agg;            // three-launch: per-tile aggregate
+    Acc *incl;           // three-launch: per-tile exclusive prefix
 };
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
-__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+template <typename Acc>
+__device__ __forceinline__ uint64_t acc_bits(Acc v) {
+    if constexpr (sizeof(Acc) == 8) {
+        uint64_t b;
+        memcpy(&b, &v, 8);
+        return b;
+    } else {
+        uint32_t b;
+        memcpy(&b, &v, 4);
+        return b;
+    }
+}
+
+template <typename Acc>
+__device__ __forceinline__ Acc acc_from_bits(uint64_t b) {
+    Acc v;
+    if constexpr (sizeof(Acc) == 8) {
+        memcpy(&v, &b, 8);
+    } else {
+        const uint32_t w = (uint32_t)b;
+        memcpy(&v, &w, 4);
+    }
+    return v;
+}
+
+template <typename Acc>
+__device__ __forceinline__ void publish(const ScanState<Acc> &st, int64_t t, Acc v,
+                                        uint32_t status) {
+    const uint64_t b = acc_bits(v);
+    st_relaxed_u64(&st.dlo[t], (b << 32) | status);
+    if constexpr (sizeof(Acc) == 8) st_relaxed_u64(&st.dhi[t], (b & 0xFFFFFFFF00000000ull) | status);
+}
+
+// status of tile t (0 while not ready or torn between A and P) and its value
+template <typename Acc>
+__device__ __forceinline__ uint32_t read_desc(const ScanState<Acc> &st, int64_t t, Acc &v) {
+    const uint64_t lo = ld_relaxed_u64(&st.dlo[t]);
+    if constexpr (sizeof(Acc) == 8) {
+        const uint64_t hi = ld_relaxed_u64(&st.dhi[t]);
+        if ((uint32_t)lo != (uint32_t)hi) return 0u;
+        v = acc_from_bits<Acc>((hi & 0xFFFFFFFF00000000ull) | (lo >> 32));
+    } else {
+        v = acc_from_bits<Acc>(lo >> 32);
+    }
+    return (uint32_t)lo;
 }
 
 template <typename Acc>
@@ -173,46 +232,51 @@ __device__ __forceinline__ Acc warp_incl_scan(Acc v, int lane) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+// exclusive warp prefix from the inclusive one (a shuffle, not incl - own: no cancellation)
+template <typename Acc>
+__device__ __forceinline__ Acc warp_excl_from_incl(Acc incl, int lane) {
+    const Acc e = __shfl_up_sync(0xffffffffu, incl, 1);
+    return lane == 0 ? Acc(0) : e;
 }
 
-// Look-back by one warp: exclusive prefix of `tile` = nearest inclusive prefix (flag 2) plus
-// the aggregates (flag 1) of the tiles after it.  Each lane inspects LB consecutive
-// predecessors per round (a window of 32*LB tiles), so a long run of aggregate-only
-// predecessors costs one L2 round trip per 32*LB tiles.  Flags are read relaxed; one gpu-scope
-// fence (acquire pattern) orders the value reads after the flags that published them.
+// Look-back by one warp: exclusive prefix of `tile` = nearest inclusive prefix (P) plus the
+// aggregates (A) of the tiles after it.  Lane l reads descriptors j - 32 m - l (m < LB), so
+// every poll is LB coalesced requests and a window covers 32 * LB predecessors; while a
+// needed predecessor is not ready the warp sleeps briefly and polls again.
 template <typename Acc, int LB>
 __device__ Acc look_back(const ScanState<Acc> &st, int64_t tile, int lane) {
     constexpr int W = 32 * LB;
     Acc prefix = 0;
     int64_t j = tile - 1;                                   // newest predecessor of the window
+    uint32_t ns = 32;
     while (true) {
         uint32_t f[LB];
+        Acc v[LB];
+#pragma unroll
+        for (int m = 0; m < LB; ++m) {
+            const int64_t t = j - (m * 32 + lane);
+            v[m] = 0;
+            f[m] = t >= 0 ? read_desc(st, t, v[m]) : 2u;
+        }
         int dp = W;                                         // distance of the nearest P
 #pragma unroll
-        for (int m = 0; m < LB; ++m) {
-            const int64_t t = j - (lane * LB + m);
-            f[m] = t >= 0 ? ld_relaxed(&st.flags[t]) : 2u;
-            if (f[m] == 2u && dp == W) dp = lane * LB + m;
-        }
-        dp = __reduce_min_sync(0xffffffffu, (uint32_t)dp);
-        bool missing = false;                               // a needed predecessor unpublished
+        for (int m = LB - 1; m >= 0; --m)
+            if (f[m] == 2u) dp = m * 32 + lane;
+        dp = (int)__reduce_min_sync(0xffffffffu, (uint32_t)dp);
+        bool missing = false;
 #pragma unroll
         for (int m = 0; m < LB; ++m)
-            if (lane * LB + m <= dp && lane * LB + m < W && f[m] == 0u) missing = true;
-        if (__any_sync(0xffffffffu, missing)) continue;
-        __threadfence();                                    // acquire: flags -> values
-        Acc v = 0;
-#pragma unroll
-        for (int m = 0; m < LB; ++m) {
-            const int d = lane * LB + m;
-            const int64_t t = j - d;
-            if (d <= dp && t >= 0) v += f[m] == 2u ? __ldcg(&st.incl[t]) : __ldcg(&st.agg[t]);
+            if (m * 32 + lane <= dp && f[m] == 0u) missing = true;
+        if (__any_sync(0xffffffffu, missing)) {
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+            continue;
         }
-        prefix += warp_sum(v);
+        Acc sum = 0;
+#pragma unroll
+        for (int m = 0; m < LB; ++m)
+            if (m * 32 + lane <= dp) sum += v[m];
+        prefix += warp_sum(sum);
         if (dp < W) return prefix;
         j -= W;
     }
@@ -285,25 +349,16 @@ scan_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
         if (w < warp) wpre += warp_tot[w];
         agg += warp_tot[w];
     }
-    const Acc texcl = wpre + wincl - tsum;                     // exclusive prefix in the tile
+    const Acc texcl = wpre + warp_excl_from_incl(wincl, lane);  // exclusive prefix in the tile
 
     if (warp == 0) {
         Acc prefix = 0;
         if (tile == 0) {
-            if (lane == 0) {
-                st.incl[0] = agg;
-                st_release(&st.flags[0], 2u);
-            }
+            if (lane == 0) publish(st, 0, agg, 2u);
         } else {
-            if (lane == 0) {
-                st.agg[tile] = agg;
-                st_release(&st.flags[tile], 1u);
-            }
-            prefix = look_back<Acc, 16>(st, tile, lane);
-            if (lane == 0) {
-                st.incl[tile] = prefix + agg;
-                st_release(&st.flags[tile], 2u);
-            }
+            if (lane == 0) publish(st, tile, agg, 1u);
+            prefix = look_back<Acc, 4>(st, tile, lane);      // 4: no spills at 64 registers
+            if (lane == 0) publish(st, tile, prefix + agg, 2u);
         }
         if (lane == 0) tile_prefix = prefix;
     }
@@ -416,7 +471,7 @@ scan_tiles_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n,
         const int64_t e0 = wbase + (int64_t)k * 32 * V + (int64_t)lane * V;
         const Acc ls = vec_sum<In, Acc>(raw[k]);     // recomputed: saves R accumulators
         const Acc wi = warp_incl_scan(ls, lane);
-        Acc run = rcarry + wi - ls;
+        Acc run = rcarry + warp_excl_from_incl(wi, lane);
         rcarry += __shfl_sync(0xffffffffu, wi, 31);
         uint4 o = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -431,6 +486,270 @@ scan_tiles_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n,
             for (int j = 0; j < V; ++j)
                 if (e0 + j < n) out[e0 + j] = unpack<In>(o, j);
         }
+    }
+}
+
+// ---- streaming single-pass scan (the default for long, 16-byte aligned arrays) ------------
+// Persistent, warp-specialised, one CTA per SM.  Tiles of NC * 32 * VPT 16-byte vectors are
+// claimed in order from an atomic counter; every tile passes twice through an S-stage
+// shared-memory ring of 1-D TMA bulk copies:
+//
+//   R(k)   : tile k from HBM (L2 policy evict_last) -> warp totals -> aggregate -> publish A
+//   S(k-D) : tile k-D again, now an L2 hit (evict_first) -> scan from its exclusive prefix ->
+//            16-byte coalesced stores
+//
+// so a tile's look-back has D tile-periods of slack (D * 148 tiles of L2 lookahead, 28 MB at
+// D = 4) and no aggregate ever waits on a look-back: the critical path is the HBM stream
+// (read n + write n), not the inter-CTA signalling latency, which under a saturated memory
+// system is several microseconds (measured: a look-back on the critical path held the
+// single-pass scans to 0.3-0.48 of peak).
+//
+//   producer warp   : claim tile, st.async its tag + bulk-copy its bytes onto full[s]; the
+//                     ring order is R(0..D-1), then R(k), S(k-D) pairs, then the S tail
+//   compute warps   : R items -> warp totals (st.async onto wsum[q]); S items -> wait
+//                     pfx[q], scan, store; q = k mod Q tile slots, Q = D + 1
+//   aggregator warp : wait wsum[q], aggregate, publish A (P for tile 0), forward on aggb[q]
+//   look-back warp  : wait aggb[q], look back, publish P, st.async the prefix onto pfx[q]
+//
+// Values that cross warps travel by st.async on the mbarrier their reader waits on (what
+// racecheck tracks), hence the 2-CTA cluster launch.  Progress: tiles are claimed in order
+// by running CTAs and aggregates depend on nothing but their own bytes.
+template <int NC, int VPT, int S, int D>
+struct ScanStreamCfg {
+    static constexpr int THREADS = 32 * (NC + 3);
+    static constexpr int TB = NC * 32 * VPT * 16;      // tile bytes
+    static constexpr int SMEM = S * TB;
+    static constexpr int Q = D + 1;                    // tile metadata slots
+    static_assert(D >= 1 && S >= 2, "need lookahead and a double-buffered ring");
+};
+
+constexpr uint64_t kScanSentinel = ~0ull;              // "no more tiles" tag
+
+template <typename In, int NC, int VPT, int S, int D>
+__global__ void __launch_bounds__(ScanStreamCfg<NC, VPT, S, D>::THREADS, 1)
+scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, int64_t ntiles,
+                   ScanState<typename AccOf<In>::T> st) {
+    using Acc = typename AccOf<In>::T;
+    using C = ScanStreamCfg<NC, VPT, S, D>;
+    constexpr int V = 16 / sizeof(In);              // elements per 16-byte vector
+    constexpr int TB = C::TB;
+    constexpr int Q = C::Q;
+    constexpr int64_t T = TB / sizeof(In);          // tile elements
+    constexpr int CHUNK = 16384;                    // bytes per bulk copy
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t full[S], empty[S];          // data ring
+    __shared__ __align__(8) uint64_t tag[S];                     // tile id of each ring item
+    __shared__ __align__(8) uint64_t wsum[Q], aggb[Q], pfx[Q];   // per tile slot
+    __shared__ __align__(8) uint64_t wtot[Q][NC + 1];            // warp totals + tile id
+    __shared__ __align__(8) uint64_t tagg[Q][2];                 // aggregate, tile id
+    __shared__ __align__(8) uint64_t tpre[Q];                    // exclusive prefix
+    __shared__ int64_t hist[D];                                  // producer: recent tile ids
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(ptx::smem_u32(&full[s]), 1);
+            ptx::mbar_init(ptx::smem_u32(&empty[s]), NC);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            ptx::mbar_init(ptx::smem_u32(&wsum[q]), 1);
+            ptx::mbar_init(ptx::smem_u32(&aggb[q]), 1);
+            ptx::mbar_init(ptx::smem_u32(&pfx[q]), 1);
+        }
+        ptx::fence_mbarrier_init();
+    }
+    __syncthreads();
+
+    if (warp == NC) {
+        // ------------------------------------------------------------------ producer
+        if (lane != 0) return;
+        const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
+        const int64_t nbytes = n * (int64_t)sizeof(In);
+        int item = 0;
+        // one ring item: wait for the stage, tag it, bulk-copy tile t (t < ntiles)
+        auto emit = [&](uint64_t tg, int64_t t, uint64_t pol) {
+            const int s = item % S;
+            const uint32_t ph = (uint32_t)(item / S) & 1u;
+            ++item;
+            ptx::mbar_wait(ptx::smem_u32(&empty[s]), ph ^ 1u);
+            const uint32_t fb = ptx::smem_u32(&full[s]);
+            uint32_t bytes = 0;
+            if (t >= 0) {
+                const int64_t rem = nbytes - t * (int64_t)TB;
+                bytes = (uint32_t)(rem >= TB ? TB : (rem & ~(int64_t)15));
+            }
+            ptx::mbar_arrive_expect_tx(fb, bytes + 8);
+            ptx::st_async_b64(ptx::smem_u32(&tag[s]), tg, fb);
+            const uint32_t dst = ptx::smem_u32(smem + (size_t)s * TB);
+            const uint8_t *src = reinterpret_cast<const uint8_t *>(in) + (t >= 0 ? t * (int64_t)TB : 0);
+            for (uint32_t c = 0; c < bytes; c += CHUNK)
+                ptx::bulk_load_1d(dst + c, src + c, bytes - c < CHUNK ? bytes - c : CHUNK, fb, pol);
+        };
+        int64_t K = -1;                                  // tiles this CTA got, once known
+        for (int64_t k = 0;; ++k) {
+            const int64_t j = k - D;
+            const int64_t tj = j >= 0 ? hist[j % D] : -1;    // read before slot k % D is reused
+            if (K < 0) {
+                const int64_t t =
+                    (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(st.counter), 1ull);
+                if (t >= ntiles) {
+                    K = k;
+                    emit(kScanSentinel, -1, drop);
+                } else {
+                    hist[k % D] = t;
+                    emit((uint64_t)t, t, keep);
+                }
+            }
+            if (j >= 0) {
+                if (K >= 0 && j >= K) return;
+                emit((uint64_t)tj, tj, drop);
+            }
+        }
+    }
+
+    if (warp == NC + 1) {
+        // ------------------------------------------------------------------ aggregator
+        for (int64_t k = 0;; ++k) {
+            const int q = (int)(k % Q);
+            const uint32_t ph = (uint32_t)(k / Q) & 1u;
+            const uint32_t wb = ptx::smem_u32(&wsum[q]);
+            if (lane == 0) ptx::mbar_arrive_expect_tx(wb, (NC + 1) * 8);
+            ptx::mbar_wait(wb, ph);
+            const uint64_t tg = wtot[q][NC];
+            Acc agg = 0;
+#pragma unroll
+            for (int w = 0; w < NC; ++w) agg += acc_from_bits<Acc>(wtot[q][w]);
+            if (lane == 0) {
+                if (tg != kScanSentinel) publish(st, (int64_t)tg, agg, tg == 0 ? 2u : 1u);
+                const uint32_t ab = ptx::smem_u32(&aggb[q]);
+                ptx::mbar_arrive_expect_tx(ab, 16);
+                ptx::st_async_b64(ptx::smem_u32(&tagg[q][0]), acc_bits(agg), ab);
+                ptx::st_async_b64(ptx::smem_u32(&tagg[q][1]), tg, ab);
+            }
+            if (tg == kScanSentinel) return;
+        }
+    }
+
+    if (warp == NC + 2) {
+        // ------------------------------------------------------------------ look-back
+        for (int64_t k = 0;; ++k) {
+            const int q = (int)(k % Q);
+            const uint32_t ph = (uint32_t)(k / Q) & 1u;
+            ptx::mbar_wait(ptx::smem_u32(&aggb[q]), ph);
+            const uint64_t tg = tagg[q][1];
+            if (tg == kScanSentinel) return;
+            const int64_t t = (int64_t)tg;
+            const Acc agg = acc_from_bits<Acc>(tagg[q][0]);
+            Acc prefix = 0;
+            if (t > 0) {
+                prefix = look_back<Acc, 8>(st, t, lane);
+                if (lane == 0) publish(st, t, prefix + agg, 2u);
+            }
+            if (lane == 0) {
+                const uint32_t pb = ptx::smem_u32(&pfx[q]);
+                ptx::mbar_arrive_expect_tx(pb, 8);
+                ptx::st_async_b64(ptx::smem_u32(&tpre[q]), acc_bits(prefix), pb);
+            }
+        }
+    }
+
+    // ---------------------------------------------------------------------- compute warps
+    // warp w owns vectors [w*32*VPT, (w+1)*32*VPT) of a tile, in VPT rounds of 32 consecutive
+    // 16-byte vectors (512 contiguous bytes per warp instruction, conflict-free)
+    const uint64_t drop = ptx::policy_evict_first();
+    auto load_vec = [&](uint32_t sbase, int64_t tbase, int k, uint4 &r) {
+        const int vi = (warp * VPT + k) * 32 + lane;
+        const int64_t e0 = tbase + (int64_t)vi * V;
+        if (e0 + V <= n) {
+            r = ptx::lds128(sbase + vi * 16);
+        } else {                                         // ragged tail: not bulk-copied
+            r = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if (e0 + j < n) set_elem<In>(r, j, in[e0 + j]);
+        }
+    };
+    int item = 0;
+    int64_t K = -1;
+    for (int64_t k = 0;; ++k) {
+        if (K < 0) {
+            // R(k): warp totals of tile k
+            const int s = item % S;
+            const uint32_t ph = (uint32_t)(item / S) & 1u;
+            ++item;
+            ptx::mbar_wait(ptx::smem_u32(&full[s]), ph);
+            const uint64_t tg = tag[s];
+            const int q = (int)(k % Q);
+            const uint32_t wb = ptx::smem_u32(&wsum[q]);
+            Acc wsum_v = 0;
+            if (tg != kScanSentinel) {
+                const uint32_t sbase = ptx::smem_u32(smem + (size_t)s * TB);
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) {
+                    uint4 r;
+                    load_vec(sbase, (int64_t)tg * T, v, r);
+                    wsum_v += vec_sum<In, Acc>(r);
+                }
+                wsum_v = warp_sum(wsum_v);
+            } else {
+                K = k;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
+                ptx::st_async_b64(ptx::smem_u32(&wtot[q][warp]), acc_bits(wsum_v), wb);
+                if (warp == 0) ptx::st_async_b64(ptx::smem_u32(&wtot[q][NC]), tg, wb);
+            }
+        }
+        const int64_t j = k - D;
+        if (j < 0) continue;
+        if (K >= 0 && j >= K) break;
+        // S(j): scan tile j (its bytes again, from L2) from its exclusive prefix
+        const int s = item % S;
+        const uint32_t ph = (uint32_t)(item / S) & 1u;
+        ++item;
+        const int q = (int)(j % Q);
+        const uint32_t qph = (uint32_t)(j / Q) & 1u;
+        ptx::mbar_wait(ptx::smem_u32(&wsum[q]), qph);    // warp totals (completed phase)
+        ptx::mbar_wait(ptx::smem_u32(&pfx[q]), qph);
+        ptx::mbar_wait(ptx::smem_u32(&full[s]), ph);
+        const int64_t tbase = (int64_t)tag[s] * T;
+        Acc rcarry = acc_from_bits<Acc>(tpre[q]);
+#pragma unroll
+        for (int w = 0; w < NC; ++w)
+            if (w < warp) rcarry += acc_from_bits<Acc>(wtot[q][w]);
+        const uint32_t sbase = ptx::smem_u32(smem + (size_t)s * TB);
+        uint4 raw[VPT];
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) load_vec(sbase, tbase, v, raw[v]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));   // stage reusable
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            const int vi = (warp * VPT + v) * 32 + lane;
+            const int64_t e0 = tbase + (int64_t)vi * V;
+            const Acc ls = vec_sum<In, Acc>(raw[v]);
+            const Acc wi = warp_incl_scan(ls, lane);
+            Acc run = rcarry + warp_excl_from_incl(wi, lane);
+            rcarry += __shfl_sync(0xffffffffu, wi, 31);
+            uint4 o = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                run += to_acc<Acc>(unpack<In>(raw[v], e));
+                set_elem<In>(o, e, (In)run);
+            }
+            if (e0 + V <= n) {
+                ptx::stg128_hint(out + e0, o, drop);
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    if (e0 + e < n) out[e0 + e] = unpack<In>(o, e);
+            }
+        }
+        // slot q is rewritten by R(j + Q) = R(k + 1): every compute warp is done with it first
+        ptx::named_bar_sync(1, 32 * NC);
     }
 }
 

@@ -75,8 +75,8 @@ def main():
         ok = y.cpu().numpy().view(np.uint32).tobytes() == V.materialize(small, ops).tobytes()
         bad += not ok
         print(f"view {ops}: {'ok' if ok else 'MISMATCH'}", flush=True)
-    # block reduction (thread / warp / CTA groups) and scan (single pass and, with
-    # DESC_SCAN_SINGLE_MAX_TILES=2 in the environment, the three-launch route)
+    # block reduction (thread / warp / CTA groups) and scan (every algorithm; the streaming
+    # one over a few tiles per CTA so that its stage ring wraps)
     for dt, n in ((np.int32, 100003), (np.float32, 70001), (np.int64, 50000), (np.uint8, 90000)):
         a = (synth.random_ints(n, dt, 5) if dt != np.float32 else synth.random_floats(n, dt, 5))
         x = torch.from_numpy(a).cuda()
@@ -90,13 +90,23 @@ def main():
                 ok = y.cpu().numpy().tobytes() == ref.tobytes()
             bad += not ok
             print(f"block_reduce {dt.__name__} n={n} B={B}: {'ok' if ok else 'MISMATCH'}", flush=True)
-        y = desc.scan(x, out=torch.zeros_like(x))
-        torch.cuda.synchronize()
         ref = oracle.scan(a)
-        ok = (np.allclose(y.cpu().numpy(), ref, rtol=1e-5, atol=1e-3) if dt == np.float32
-              else y.cpu().numpy().tobytes() == ref.tobytes())
-        bad += not ok
-        print(f"scan {dt.__name__} n={n}: {'ok' if ok else 'MISMATCH'}", flush=True)
+        for algo in ("lookback", "three_pass", "stream"):
+            y = desc.scan(x, out=torch.zeros_like(x), algo=algo)
+            torch.cuda.synchronize()
+            ok = (np.allclose(y.cpu().numpy(), ref, rtol=1e-5, atol=1e-3) if dt == np.float32
+                  else y.cpu().numpy().tobytes() == ref.tobytes())
+            bad += not ok
+            print(f"scan {algo} {dt.__name__} n={n}: {'ok' if ok else 'MISMATCH'}", flush=True)
+    # streaming scan, several tiles per CTA (48 KB tiles: ~10 per CTA on 148 SMs)
+    n = 148 * 10 * 12288 + 5
+    a = synth.random_ints(n, np.int32, 6)
+    x = torch.from_numpy(a).cuda()
+    y = desc.scan(x, algo="stream")
+    torch.cuda.synchronize()
+    ok = y.cpu().numpy().tobytes() == oracle.scan(a).tobytes()
+    bad += not ok
+    print(f"scan stream int32 n={n}: {'ok' if ok else 'MISMATCH'}", flush=True)
     print("sanitize driver:", "PASS" if bad == 0 else f"{bad} FAILURES")
     return 1 if bad else 0
 

@@ -60,30 +60,59 @@ def test_block_reduce(dt, n, B):
             assert np.all(np.abs(got.astype(np.float64) - ref) <= tol), (n, B, offset)
 
 
+def _check_scan(got, a, dt, what):
+    ref = oracle.scan(a)
+    if dt in INTS:
+        assert got.tobytes() == ref.tobytes(), what
+    else:
+        absx = oracle.scan(np.abs(a).astype(np.float64))
+        tol = _ulp(dt, ref) + 2.0 * np.arange(1, a.size + 1) * 2.0 ** -53 * absx
+        assert np.all(np.abs(got.astype(np.float64) - ref) <= tol), what
+
+
+@pytest.mark.parametrize("algo", ["auto", "lookback", "three_pass", "stream"])
 @pytest.mark.parametrize("dt", INTS + FLOATS)
-@pytest.mark.parametrize("n", [1, 255, 4096, 4097, 100003, (1 << 22) + 3])
-def test_scan(dt, n):
+@pytest.mark.parametrize("n", [1, 15, 255, 4096, 4097, 100003, (1 << 22) + 3])
+def test_scan(dt, n, algo):
     for offset in (0, 1):
         a = _input(n, dt, n + offset)
         x = _dev(a, offset)
-        y = desc.scan(x)
+        misaligned = (x.data_ptr() % 16) != 0
+        if algo == "stream" and misaligned:
+            with pytest.raises(desc.DescError, match="KERNEL"):
+                desc.scan(x, algo=algo)
+            continue
+        y = desc.scan(x, algo=algo)
         torch.cuda.synchronize()
-        got = y.cpu().numpy()
-        ref = oracle.scan(a)
-        if dt in INTS:
-            assert got.tobytes() == ref.tobytes(), (n, offset)
-        else:
-            absx = oracle.scan(np.abs(a).astype(np.float64))
-            tol = _ulp(dt, ref) + 2.0 * np.arange(1, n + 1) * 2.0 ** -53 * absx
-            assert np.all(np.abs(got.astype(np.float64) - ref) <= tol), (n, offset)
+        _check_scan(y.cpu().numpy(), a, dt, (n, offset, algo))
+
+
+@pytest.mark.parametrize("dt", INTS + FLOATS)
+def test_scan_stream_many_tiles_per_cta(dt):
+    """Long enough that every persistent CTA streams several tiles through each stage, with a
+    ragged tail (not a multiple of 16 bytes); also the AUTO choice at this size."""
+    n = (1 << 25) + 7 if np.dtype(dt).itemsize <= 4 else (1 << 24) + 7
+    a = _input(n, dt, 99)
+    x = torch.from_numpy(a).cuda()
+    for algo in ("stream", "auto"):
+        y = desc.scan(x, algo=algo)
+        torch.cuda.synchronize()
+        assert desc.desc_last_launch_count() == 1
+        _check_scan(y.cpu().numpy(), a, dt, algo)
 
 
 def test_scan_in_place_and_repeat():
     a = synth.random_ints(1 << 20, np.int32, 4)
     x = torch.from_numpy(a).cuda()
     work = torch.empty(desc.desc_scan_workspace(a.size, "i32"), dtype=torch.uint8, device="cuda")
-    for _ in range(3):          # workspace reused: the call re-zeroes the tile state
-        y = desc.scan(x, work=work)
+    for algo in ("auto", "lookback", "three_pass", "stream"):
+        for _ in range(3):      # workspace reused: the call re-zeroes the tile state
+            y = desc.scan(x, work=work, algo=algo)
+    for algo in ("lookback", "three_pass", "stream"):
+        z = x.clone()
+        desc.scan(z, out=z, work=work, algo=algo)   # in place
+        torch.cuda.synchronize()
+        assert z.cpu().numpy().tobytes() == oracle.scan(a).tobytes(), algo
     desc.scan(x, out=x, work=work)     # in place
     torch.cuda.synchronize()
     assert x.cpu().numpy().tobytes() == oracle.scan(a).tobytes()
@@ -102,3 +131,6 @@ def test_errors():
         desc.scan(y, work=work)
     with pytest.raises(desc.DescError, match="ALIAS"):
         desc.desc_scan(y.data_ptr(), y.data_ptr() + 4, 50, "f32", work.data_ptr(), 1 << 20)
+    big = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    with pytest.raises(desc.DescError, match="KERNEL"):
+        desc.desc_scan_ex(y.data_ptr(), y.data_ptr(), 100, "f32", big.data_ptr(), 1 << 20, 9)
