@@ -1110,7 +1110,8 @@ int64_t scan_workspace_bytes(int64_t n, int es) {
 }
 
 // streaming scan: 16 compute warps x 32 lanes x 6 16-byte vectors = 48 KB tiles, a 4-stage
-// shared-memory ring (192 KB), lookahead 4 (tile k+4 is reduced before tile k is scanned)
+// shared-memory ring (192 KB), lookahead 4 (tile k+4 is reduced before tile k is scanned;
+// 5 tiles x 96 columns parked in TMEM)
 #ifndef DESC_SCAN_VPT        // compile-time overrides: A/B builds only
 #define DESC_SCAN_VPT 6
 #endif
@@ -1120,9 +1121,12 @@ int64_t scan_workspace_bytes(int64_t n, int es) {
 #ifndef DESC_SCAN_LOOKAHEAD
 #define DESC_SCAN_LOOKAHEAD 4
 #endif
-constexpr int kScanNC = 16, kScanVpt = DESC_SCAN_VPT, kScanStages = DESC_SCAN_STAGES,
-              kScanLookahead = DESC_SCAN_LOOKAHEAD;
-using ScanStreamC = desc::ScanStreamCfg<kScanNC, kScanVpt, kScanStages, kScanLookahead>;
+// (bytes: 3 vectors per lane -- 16 elements per vector would spill at 6 -- in 8 stages)
+constexpr int kScanNC = 16, kScanLookahead = DESC_SCAN_LOOKAHEAD;
+constexpr int scan_vpt(int es) { return es == 1 ? 3 : DESC_SCAN_VPT; }
+constexpr int scan_stages(int es) { return es == 1 ? 8 : DESC_SCAN_STAGES; }
+template <int ES>
+using ScanStreamC = desc::ScanStreamCfg<kScanNC, scan_vpt(ES), scan_stages(ES), kScanLookahead>;
 
 template <typename In, int ITEMS>
 desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool vec,
@@ -1151,7 +1155,8 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     if (desc_status s = device_info(dev, &di)) return s;
     // streaming tiles (96 KB) are never more than the look-back tiles (<= 32 KB), so the
     // workspace sized by scan_tiles() covers both
-    constexpr int64_t TBY = ScanStreamC::TB;
+    using SC = ScanStreamC<(int)sizeof(In)>;
+    constexpr int64_t TBY = SC::TB;
     const int64_t ts = (n * es + TBY - 1) / TBY;
     if (algo == DESC_SCAN_AUTO) {
         static const int single_max = dev_knob("DESC_SCAN_SINGLE_MAX_TILES", 256);
@@ -1161,15 +1166,16 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     }
     if (algo == DESC_SCAN_STREAM) {
         if (!vec) return fail(DESC_ERR_KERNEL, "streaming scan needs 16-byte aligned in and out");
-        auto kern = desc::scan_stream_kernel<In, kScanNC, kScanVpt, kScanStages, kScanLookahead>;
-        const int smem = ScanStreamC::SMEM;
+        auto kern = desc::scan_stream_kernel<In, kScanNC, scan_vpt(sizeof(In)),
+                                             scan_stages(sizeof(In)), kScanLookahead>;
+        const int smem = SC::SMEM;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute (scan)");
         st.dhi = reinterpret_cast<uint64_t *>(work + 256 + round_up(ts * 8, 256));
         e = cudaMemsetAsync(work, 0, 256 + desc_words * round_up(ts * 8, 256), stream);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (scan state)");
         const int64_t grid = ts < di.sms ? ts : di.sms;
-        e = launch_cluster2(kern, (int)grid, ScanStreamC::THREADS, smem, stream, pi, po, n, ts, st);
+        e = launch_cluster2(kern, (int)grid, SC::THREADS, smem, stream, pi, po, n, ts, st);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "scan_stream launch");
         g_last_launches = 1;

@@ -491,39 +491,54 @@ scan_tiles_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n,
 
 // ---- streaming single-pass scan (the default for long, 16-byte aligned arrays) ------------
 // Persistent, warp-specialised, one CTA per SM.  Tiles of NC * 32 * VPT 16-byte vectors are
-// claimed in order from an atomic counter; every tile passes twice through an S-stage
-// shared-memory ring of 1-D TMA bulk copies:
+// claimed in order from an atomic counter and read from HBM exactly once, through an S-stage
+// shared-memory ring of 1-D TMA bulk copies.  Each tile is handled twice by the compute
+// warps, D tiles apart:
 //
-//   R(k)   : tile k from HBM (L2 policy evict_last) -> warp totals -> aggregate -> publish A
-//   S(k-D) : tile k-D again, now an L2 hit (evict_first) -> scan from its exclusive prefix ->
-//            16-byte coalesced stores
+//   R(k)   : stage -> registers -> warp totals -> aggregate -> publish A; the registers are
+//            parked in tensor memory (TMEM, 256 KB per SM, otherwise idle here) and the
+//            stage is released at once
+//   S(k-D) : TMEM -> registers -> scan from the tile's exclusive prefix -> 16-byte coalesced
+//            stores (2 n bytes of HBM traffic in all)
 //
-// so a tile's look-back has D tile-periods of slack (D * 148 tiles of L2 lookahead, 28 MB at
-// D = 4) and no aggregate ever waits on a look-back: the critical path is the HBM stream
-// (read n + write n), not the inter-CTA signalling latency, which under a saturated memory
-// system is several microseconds (measured: a look-back on the critical path held the
-// single-pass scans to 0.3-0.48 of peak).
+// so a tile's look-back has D tile-periods of slack and no aggregate ever waits on a
+// look-back: the critical path is the HBM stream, not the inter-CTA signalling latency,
+// which under a saturated memory system is several microseconds (measured: a look-back on
+// the critical path held single-pass scans to 0.3-0.5 of peak; re-reading the lookahead
+// tiles from L2 instead of TMEM cost ~15% more).
 //
-//   producer warp   : claim tile, st.async its tag + bulk-copy its bytes onto full[s]; the
-//                     ring order is R(0..D-1), then R(k), S(k-D) pairs, then the S tail
-//   compute warps   : R items -> warp totals (st.async onto wsum[q]); S items -> wait
-//                     pfx[q], scan, store; q = k mod Q tile slots, Q = D + 1
+//   producer warp   : claim tile, st.async its tag + bulk-copy its bytes onto full[s]
+//   compute warps   : R(k) and S(k-D) per iteration; warp w owns vectors
+//                     [w*32*VPT, (w+1)*32*VPT) of a tile in VPT rounds of 32 consecutive
+//                     16-byte vectors (512 contiguous bytes per warp instruction) and parks
+//                     them in its own TMEM lane quarter (w % 4) and column block
 //   aggregator warp : wait wsum[q], aggregate, publish A (P for tile 0), forward on aggb[q]
 //   look-back warp  : wait aggb[q], look back, publish P, st.async the prefix onto pfx[q]
 //
 // Values that cross warps travel by st.async on the mbarrier their reader waits on (what
-// racecheck tracks), hence the 2-CTA cluster launch.  Progress: tiles are claimed in order
-// by running CTAs and aggregates depend on nothing but their own bytes.
+// racecheck tracks), hence the 2-CTA cluster launch.  Tile metadata slots q = k mod Q with
+// Q = S + D + 2: a compute warp can run at most S ring items ahead of the slowest one, so a
+// slot is never rewritten while a slow warp still reads it.  Progress: tiles are claimed in
+// order by running CTAs and aggregates depend on nothing but their own bytes.
 template <int NC, int VPT, int S, int D>
 struct ScanStreamCfg {
     static constexpr int THREADS = 32 * (NC + 3);
     static constexpr int TB = NC * 32 * VPT * 16;      // tile bytes
     static constexpr int SMEM = S * TB;
-    static constexpr int Q = D + 1;                    // tile metadata slots
+    static constexpr int Q = S + D + 2;                // tile metadata slots
+    static constexpr int QT = D + 1;                   // tiles parked in TMEM per warp
+    static constexpr int WCOLS = 4 * VPT;              // TMEM columns per warp per tile
+    static constexpr int TCOLS = (NC / 4) * WCOLS;     // TMEM columns per tile
     static_assert(D >= 1 && S >= 2, "need lookahead and a double-buffered ring");
+    static_assert(NC % 4 == 0, "compute warps cover the four TMEM lane quarters evenly");
+    static_assert(QT * TCOLS <= 512, "parked tiles must fit the 512 TMEM columns");
 };
 
 constexpr uint64_t kScanSentinel = ~0ull;              // "no more tiles" tag
+
+#ifndef DESC_SCAN_DIAG        // diagnostics builds only (wrong results): 1 = no look-back,
+#define DESC_SCAN_DIAG 0      // 2 = outputs are the inputs (no scan arithmetic)
+#endif
 
 template <typename In, int NC, int VPT, int S, int D>
 __global__ void __launch_bounds__(ScanStreamCfg<NC, VPT, S, D>::THREADS, 1)
@@ -543,7 +558,7 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
     __shared__ __align__(8) uint64_t wtot[Q][NC + 1];            // warp totals + tile id
     __shared__ __align__(8) uint64_t tagg[Q][2];                 // aggregate, tile id
     __shared__ __align__(8) uint64_t tpre[Q];                    // exclusive prefix
-    __shared__ int64_t hist[D];                                  // producer: recent tile ids
+    __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     if (tid == 0) {
@@ -560,52 +575,36 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
         }
         ptx::fence_mbarrier_init();
     }
+    if (warp == 0) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 512);
+    ptx::tmem_fence_before_sync();
     __syncthreads();
+    ptx::tmem_fence_after_sync();
 
     if (warp == NC) {
         // ------------------------------------------------------------------ producer
         if (lane != 0) return;
-        const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
+        const uint64_t pol = ptx::policy_evict_first();
         const int64_t nbytes = n * (int64_t)sizeof(In);
-        int item = 0;
-        // one ring item: wait for the stage, tag it, bulk-copy tile t (t < ntiles)
-        auto emit = [&](uint64_t tg, int64_t t, uint64_t pol) {
-            const int s = item % S;
-            const uint32_t ph = (uint32_t)(item / S) & 1u;
-            ++item;
+        for (int64_t k = 0;; ++k) {
+            const int s = (int)(k % S);
+            const uint32_t ph = (uint32_t)(k / S) & 1u;
             ptx::mbar_wait(ptx::smem_u32(&empty[s]), ph ^ 1u);
+            const int64_t t =
+                (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(st.counter), 1ull);
             const uint32_t fb = ptx::smem_u32(&full[s]);
-            uint32_t bytes = 0;
-            if (t >= 0) {
-                const int64_t rem = nbytes - t * (int64_t)TB;
-                bytes = (uint32_t)(rem >= TB ? TB : (rem & ~(int64_t)15));
+            if (t >= ntiles) {                           // no more tiles: tell the consumers
+                ptx::mbar_arrive_expect_tx(fb, 8);
+                ptx::st_async_b64(ptx::smem_u32(&tag[s]), kScanSentinel, fb);
+                return;
             }
+            const int64_t rem = nbytes - t * (int64_t)TB;
+            const uint32_t bytes = (uint32_t)(rem >= TB ? TB : (rem & ~(int64_t)15));
             ptx::mbar_arrive_expect_tx(fb, bytes + 8);
-            ptx::st_async_b64(ptx::smem_u32(&tag[s]), tg, fb);
+            ptx::st_async_b64(ptx::smem_u32(&tag[s]), (uint64_t)t, fb);
             const uint32_t dst = ptx::smem_u32(smem + (size_t)s * TB);
-            const uint8_t *src = reinterpret_cast<const uint8_t *>(in) + (t >= 0 ? t * (int64_t)TB : 0);
+            const uint8_t *src = reinterpret_cast<const uint8_t *>(in) + t * (int64_t)TB;
             for (uint32_t c = 0; c < bytes; c += CHUNK)
                 ptx::bulk_load_1d(dst + c, src + c, bytes - c < CHUNK ? bytes - c : CHUNK, fb, pol);
-        };
-        int64_t K = -1;                                  // tiles this CTA got, once known
-        for (int64_t k = 0;; ++k) {
-            const int64_t j = k - D;
-            const int64_t tj = j >= 0 ? hist[j % D] : -1;    // read before slot k % D is reused
-            if (K < 0) {
-                const int64_t t =
-                    (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(st.counter), 1ull);
-                if (t >= ntiles) {
-                    K = k;
-                    emit(kScanSentinel, -1, drop);
-                } else {
-                    hist[k % D] = t;
-                    emit((uint64_t)t, t, keep);
-                }
-            }
-            if (j >= 0) {
-                if (K >= 0 && j >= K) return;
-                emit((uint64_t)tj, tj, drop);
-            }
         }
     }
 
@@ -643,10 +642,12 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
             const int64_t t = (int64_t)tg;
             const Acc agg = acc_from_bits<Acc>(tagg[q][0]);
             Acc prefix = 0;
+#if !(DESC_SCAN_DIAG & 1)
             if (t > 0) {
                 prefix = look_back<Acc, 8>(st, t, lane);
                 if (lane == 0) publish(st, t, prefix + agg, 2u);
             }
+#endif
             if (lane == 0) {
                 const uint32_t pb = ptx::smem_u32(&pfx[q]);
                 ptx::mbar_arrive_expect_tx(pb, 8);
@@ -656,41 +657,39 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
     }
 
     // ---------------------------------------------------------------------- compute warps
-    // warp w owns vectors [w*32*VPT, (w+1)*32*VPT) of a tile, in VPT rounds of 32 consecutive
-    // 16-byte vectors (512 contiguous bytes per warp instruction, conflict-free)
     const uint64_t drop = ptx::policy_evict_first();
-    auto load_vec = [&](uint32_t sbase, int64_t tbase, int k, uint4 &r) {
-        const int vi = (warp * VPT + k) * 32 + lane;
-        const int64_t e0 = tbase + (int64_t)vi * V;
-        if (e0 + V <= n) {
-            r = ptx::lds128(sbase + vi * 16);
-        } else {                                         // ragged tail: not bulk-copied
-            r = make_uint4(0, 0, 0, 0);
-#pragma unroll
-            for (int j = 0; j < V; ++j)
-                if (e0 + j < n) set_elem<In>(r, j, in[e0 + j]);
-        }
-    };
-    int item = 0;
-    int64_t K = -1;
+    // this warp's TMEM: lane quarter warp % 4, column block (warp / 4) * WCOLS of each slot
+    const uint32_t tmem_w = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) +
+                            (uint32_t)((warp >> 2) * C::WCOLS);
+    int64_t K = -1;                                      // tiles this CTA got, once known
     for (int64_t k = 0;; ++k) {
         if (K < 0) {
-            // R(k): warp totals of tile k
-            const int s = item % S;
-            const uint32_t ph = (uint32_t)(item / S) & 1u;
-            ++item;
+            // R(k): warp total of tile k; its vectors parked in TMEM slot k % QT
+            const int s = (int)(k % S);
+            const uint32_t ph = (uint32_t)(k / S) & 1u;
             ptx::mbar_wait(ptx::smem_u32(&full[s]), ph);
             const uint64_t tg = tag[s];
             const int q = (int)(k % Q);
-            const uint32_t wb = ptx::smem_u32(&wsum[q]);
             Acc wsum_v = 0;
             if (tg != kScanSentinel) {
+                const int64_t tbase = (int64_t)tg * T;
                 const uint32_t sbase = ptx::smem_u32(smem + (size_t)s * TB);
+                const uint32_t tm = tmem_w + (uint32_t)((k % C::QT) * C::TCOLS);
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
+                    const int vi = (warp * VPT + v) * 32 + lane;
+                    const int64_t e0 = tbase + (int64_t)vi * V;
                     uint4 r;
-                    load_vec(sbase, (int64_t)tg * T, v, r);
+                    if (e0 + V <= n) {
+                        r = ptx::lds128(sbase + vi * 16);
+                    } else {                             // ragged tail: not bulk-copied
+                        r = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                        for (int e = 0; e < V; ++e)
+                            if (e0 + e < n) set_elem<In>(r, e, in[e0 + e]);
+                    }
                     wsum_v += vec_sum<In, Acc>(r);
+                    ptx::tmem_st4(tm + 4 * v, r);
                 }
                 wsum_v = warp_sum(wsum_v);
             } else {
@@ -698,7 +697,8 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
             }
             __syncwarp();
             if (lane == 0) {
-                ptx::mbar_arrive(ptx::smem_u32(&empty[s]));
+                ptx::mbar_arrive(ptx::smem_u32(&empty[s]));             // stage reusable
+                const uint32_t wb = ptx::smem_u32(&wsum[q]);
                 ptx::st_async_b64(ptx::smem_u32(&wtot[q][warp]), acc_bits(wsum_v), wb);
                 if (warp == 0) ptx::st_async_b64(ptx::smem_u32(&wtot[q][NC]), tg, wb);
             }
@@ -706,26 +706,25 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
         const int64_t j = k - D;
         if (j < 0) continue;
         if (K >= 0 && j >= K) break;
-        // S(j): scan tile j (its bytes again, from L2) from its exclusive prefix
-        const int s = item % S;
-        const uint32_t ph = (uint32_t)(item / S) & 1u;
-        ++item;
+        // S(j): scan tile j from its exclusive prefix, vectors back from TMEM
         const int q = (int)(j % Q);
         const uint32_t qph = (uint32_t)(j / Q) & 1u;
         ptx::mbar_wait(ptx::smem_u32(&wsum[q]), qph);    // warp totals (completed phase)
         ptx::mbar_wait(ptx::smem_u32(&pfx[q]), qph);
-        ptx::mbar_wait(ptx::smem_u32(&full[s]), ph);
-        const int64_t tbase = (int64_t)tag[s] * T;
+        const int64_t tbase = (int64_t)wtot[q][NC] * T;
         Acc rcarry = acc_from_bits<Acc>(tpre[q]);
 #pragma unroll
         for (int w = 0; w < NC; ++w)
             if (w < warp) rcarry += acc_from_bits<Acc>(wtot[q][w]);
-        const uint32_t sbase = ptx::smem_u32(smem + (size_t)s * TB);
+        ptx::tmem_wait_st();                             // R's parking stores complete
+        const uint32_t tm = tmem_w + (uint32_t)((j % C::QT) * C::TCOLS);
         uint4 raw[VPT];
 #pragma unroll
-        for (int v = 0; v < VPT; ++v) load_vec(sbase, tbase, v, raw[v]);
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[s]));   // stage reusable
+        for (int v = 0; v < VPT; ++v) raw[v] = ptx::tmem_ld4(tm + 4 * v);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)                    // registers valid only after the wait
+            asm volatile("" : "+r"(raw[v].x), "+r"(raw[v].y), "+r"(raw[v].z), "+r"(raw[v].w));
 #pragma unroll
         for (int v = 0; v < VPT; ++v) {
             const int vi = (warp * VPT + v) * 32 + lane;
@@ -740,6 +739,9 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
                 run += to_acc<Acc>(unpack<In>(raw[v], e));
                 set_elem<In>(o, e, (In)run);
             }
+#if DESC_SCAN_DIAG & 2
+            o = raw[v];
+#endif
             if (e0 + V <= n) {
                 ptx::stg128_hint(out + e0, o, drop);
             } else {
@@ -748,8 +750,13 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
                     if (e0 + e < n) out[e0 + e] = unpack<In>(o, e);
             }
         }
-        // slot q is rewritten by R(j + Q) = R(k + 1): every compute warp is done with it first
-        ptx::named_bar_sync(1, 32 * NC);
+    }
+    // release TMEM: every compute warp is done with its columns
+    ptx::tmem_fence_before_sync();
+    ptx::named_bar_sync(1, 32 * NC);
+    if (warp == 0) {
+        ptx::tmem_fence_after_sync();
+        ptx::tmem_dealloc(tmem_base, 512);
     }
 }
 

@@ -1,0 +1,19 @@
+"""Compile-time variants of the streaming scan for A/B runs (DESC_LIB=<path>)."""
+import os, sys
+from concurrent.futures import ThreadPoolExecutor
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2305_03448_b200 import build as B
+
+VARIANTS = {
+    "diag1": ["DESC_SCAN_DIAG=1"],
+    "diag3": ["DESC_SCAN_DIAG=3"],
+    "d3": ["DESC_SCAN_LOOKAHEAD=3"],
+    "s3": ["DESC_SCAN_STAGES=3"],
+    "v4d6": ["DESC_SCAN_VPT=4", "DESC_SCAN_LOOKAHEAD=6", "DESC_SCAN_STAGES=6"],
+    "v5d5": ["DESC_SCAN_VPT=5", "DESC_SCAN_LOOKAHEAD=5", "DESC_SCAN_STAGES=5"],
+}
+out_dir = os.path.join(B.ROOT, "build_variants")
+os.makedirs(out_dir, exist_ok=True)
+with ThreadPoolExecutor(len(VARIANTS)) as ex:
+    for name, p in zip(VARIANTS, ex.map(lambda kv: B.build(defines=kv[1], out=os.path.join(out_dir, f"lib_{kv[0]}.so")), VARIANTS.items())):
+        print(name, p)
