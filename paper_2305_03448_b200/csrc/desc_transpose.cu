@@ -1109,24 +1109,27 @@ int64_t scan_workspace_bytes(int64_t n, int es) {
     return 256 + (single > three ? single : three);
 }
 
-// streaming scan: 16 compute warps x 32 lanes x 6 16-byte vectors = 48 KB tiles, a 4-stage
-// shared-memory ring (192 KB), lookahead 4 (tile k+4 is reduced before tile k is scanned;
-// 5 tiles x 96 columns parked in TMEM)
+// streaming scan: 8 reduce + 8 scan warps, tiles of 8 x 32 lanes x 12 16-byte vectors =
+// 48 KB, a 4-stage shared-memory ring (192 KB), 5 tiles (5 x 96 columns) parked in TMEM
 #ifndef DESC_SCAN_VPT        // compile-time overrides: A/B builds only
-#define DESC_SCAN_VPT 6
+#define DESC_SCAN_VPT 12
 #endif
 #ifndef DESC_SCAN_STAGES
 #define DESC_SCAN_STAGES 4
 #endif
-#ifndef DESC_SCAN_LOOKAHEAD
-#define DESC_SCAN_LOOKAHEAD 4
+#ifndef DESC_SCAN_TMEM_SLOTS
+#define DESC_SCAN_TMEM_SLOTS 5
 #endif
-// (bytes: 3 vectors per lane -- 16 elements per vector would spill at 6 -- in 8 stages)
-constexpr int kScanNC = 16, kScanLookahead = DESC_SCAN_LOOKAHEAD;
-constexpr int scan_vpt(int es) { return es == 1 ? 3 : DESC_SCAN_VPT; }
+#ifndef DESC_SCAN_LB_WARPS
+#define DESC_SCAN_LB_WARPS 1
+#endif
+// (bytes: 6 vectors per lane -- 16 elements per vector -- in 8 stages)
+constexpr int kScanNR = 8;
+constexpr int scan_vpt(int es) { return es == 1 ? 6 : DESC_SCAN_VPT; }
 constexpr int scan_stages(int es) { return es == 1 ? 8 : DESC_SCAN_STAGES; }
 template <int ES>
-using ScanStreamC = desc::ScanStreamCfg<kScanNC, scan_vpt(ES), scan_stages(ES), kScanLookahead>;
+using ScanStreamC = desc::ScanStreamCfg<kScanNR, scan_vpt(ES), scan_stages(ES),
+                                        DESC_SCAN_TMEM_SLOTS, DESC_SCAN_LB_WARPS>;
 
 template <typename In, int ITEMS>
 desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool vec,
@@ -1166,8 +1169,9 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     }
     if (algo == DESC_SCAN_STREAM) {
         if (!vec) return fail(DESC_ERR_KERNEL, "streaming scan needs 16-byte aligned in and out");
-        auto kern = desc::scan_stream_kernel<In, kScanNC, scan_vpt(sizeof(In)),
-                                             scan_stages(sizeof(In)), kScanLookahead>;
+        auto kern = desc::scan_stream_kernel<In, kScanNR, scan_vpt(sizeof(In)),
+                                             scan_stages(sizeof(In)), DESC_SCAN_TMEM_SLOTS,
+                                             DESC_SCAN_LB_WARPS>;
         const int smem = SC::SMEM;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute (scan)");
@@ -1257,6 +1261,13 @@ desc_status desc_scan(const void *in, void *out, int64_t n, desc_dtype dtype, vo
     return run_scan(in, out, n, dtype, d_work, work_bytes, DESC_SCAN_AUTO,
                     static_cast<cudaStream_t>(stream));
 }
+
+#ifdef DESC_SCAN_TRACE
+// diagnostics builds only (not in the header): copy the per-tile trace stamps to the host
+int desc_scan_trace_copy(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, desc::g_scan_trace, bytes);
+}
+#endif
 
 desc_status desc_scan_ex(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
                          size_t work_bytes, desc_scan_algo algo, void *stream) {

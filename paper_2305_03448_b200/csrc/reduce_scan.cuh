@@ -232,6 +232,20 @@ __device__ __forceinline__ Acc warp_incl_scan(Acc v, int lane) {
     return v;
 }
 
+// N independent inclusive warp scans, level by level (N shuffle chains in flight at once)
+template <typename Acc, int N>
+__device__ __forceinline__ void warp_incl_scan_n(Acc (&v)[N], int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        Acc t[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) t[i] = __shfl_up_sync(0xffffffffu, v[i], o);
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+            if (lane >= o) v[i] += t[i];
+    }
+}
+
 // exclusive warp prefix from the inclusive one (a shuffle, not incl - own: no cancellation)
 template <typename Acc>
 __device__ __forceinline__ Acc warp_excl_from_incl(Acc incl, int lane) {
@@ -244,12 +258,13 @@ __device__ __forceinline__ Acc warp_excl_from_incl(Acc incl, int lane) {
 // every poll is LB coalesced requests and a window covers 32 * LB predecessors; while a
 // needed predecessor is not ready the warp sleeps briefly and polls again.
 template <typename Acc, int LB>
-__device__ Acc look_back(const ScanState<Acc> &st, int64_t tile, int lane) {
+__device__ Acc look_back(const ScanState<Acc> &st, int64_t tile, int lane, int *polls = nullptr) {
     constexpr int W = 32 * LB;
     Acc prefix = 0;
     int64_t j = tile - 1;                                   // newest predecessor of the window
     uint32_t ns = 32;
     while (true) {
+        if (polls) ++*polls;
         uint32_t f[LB];
         Acc v[LB];
 #pragma unroll
@@ -490,72 +505,89 @@ scan_tiles_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n,
 }
 
 // ---- streaming single-pass scan (the default for long, 16-byte aligned arrays) ------------
-// Persistent, warp-specialised, one CTA per SM.  Tiles of NC * 32 * VPT 16-byte vectors are
+// Persistent, warp-specialised, one CTA per SM.  Tiles of NR * 32 * VPT 16-byte vectors are
 // claimed in order from an atomic counter and read from HBM exactly once, through an S-stage
-// shared-memory ring of 1-D TMA bulk copies.  Each tile is handled twice by the compute
-// warps, D tiles apart:
+// shared-memory ring of 1-D TMA bulk copies.  Two warp groups handle every tile:
 //
-//   R(k)   : stage -> registers -> warp totals -> aggregate -> publish A; the registers are
-//            parked in tensor memory (TMEM, 256 KB per SM, otherwise idle here) and the
-//            stage is released at once
-//   S(k-D) : TMEM -> registers -> scan from the tile's exclusive prefix -> 16-byte coalesced
-//            stores (2 n bytes of HBM traffic in all)
+//   reduce warps (NR) : stage -> registers -> warp totals (st.async onto wsum[q]); the
+//                       registers are parked in tensor memory (TMEM, 256 KB per SM, idle in
+//                       this kernel otherwise) and the stage is released at once
+//   scan warps (NR)   : wait the tile's exclusive prefix, TMEM -> registers -> scan ->
+//                       16-byte coalesced stores (2 n bytes of HBM traffic in all)
+//   producer warp     : claim tile, st.async its tag + bulk-copy its bytes onto full[s]
+//   aggregator warp   : wait wsum[q], aggregate, publish A (P for tile 0), forward on aggb[q]
+//   look-back warps   : wait aggb[q], look back, publish P, st.async the prefix onto pfx[q]
 //
-// so a tile's look-back has D tile-periods of slack and no aggregate ever waits on a
-// look-back: the critical path is the HBM stream, not the inter-CTA signalling latency,
-// which under a saturated memory system is several microseconds (measured: a look-back on
-// the critical path held single-pass scans to 0.3-0.5 of peak; re-reading the lookahead
-// tiles from L2 instead of TMEM cost ~15% more).
+// The reduce warps only wait for bytes (and a free TMEM slot), so every aggregate is
+// published as soon as its tile lands and up to QT tiles can wait for their look-backs at
+// once: the critical path is the HBM stream, not the inter-CTA signalling latency, which
+// under a saturated memory system is several microseconds.  Measured on the way here: a
+// look-back on the critical path held single-pass scans to 0.3-0.5 of peak; re-reading the
+// waiting tiles from L2 instead of TMEM cost ~15%; one warp group doing both phases coupled
+// each aggregate to an older tile's look-back.
 //
-//   producer warp   : claim tile, st.async its tag + bulk-copy its bytes onto full[s]
-//   compute warps   : R(k) and S(k-D) per iteration; warp w owns vectors
-//                     [w*32*VPT, (w+1)*32*VPT) of a tile in VPT rounds of 32 consecutive
-//                     16-byte vectors (512 contiguous bytes per warp instruction) and parks
-//                     them in its own TMEM lane quarter (w % 4) and column block
-//   aggregator warp : wait wsum[q], aggregate, publish A (P for tile 0), forward on aggb[q]
-//   look-back warp  : wait aggb[q], look back, publish P, st.async the prefix onto pfx[q]
-//
+// Reduce warp r and scan warp NR + r own the same 32 * VPT vectors of a tile (512 contiguous
+// bytes per warp instruction) and the same TMEM lane quarter (r % 4) and column block.
 // Values that cross warps travel by st.async on the mbarrier their reader waits on (what
-// racecheck tracks), hence the 2-CTA cluster launch.  Tile metadata slots q = k mod Q with
-// Q = S + D + 2: a compute warp can run at most S ring items ahead of the slowest one, so a
-// slot is never rewritten while a slow warp still reads it.  Progress: tiles are claimed in
+// racecheck tracks), hence the 2-CTA cluster launch; TMEM hand-offs use parked[qt] / freed[qt]
+// with the tcgen05 thread-sync fences.  Metadata slots q = k mod Q, Q = QT + S + 2: reduce
+// warps run at most QT tiles ahead of the scan warps (TMEM slots) and S ring items ahead of
+// each other, so a slot is never rewritten while it is read.  Progress: tiles are claimed in
 // order by running CTAs and aggregates depend on nothing but their own bytes.
-template <int NC, int VPT, int S, int D>
+template <int NR, int VPT, int S, int QT, int NLB>
 struct ScanStreamCfg {
-    static constexpr int THREADS = 32 * (NC + 3);
-    static constexpr int TB = NC * 32 * VPT * 16;      // tile bytes
+    static constexpr int THREADS = 32 * (2 * NR + 2 + NLB);
+    static constexpr int TB = NR * 32 * VPT * 16;      // tile bytes
     static constexpr int SMEM = S * TB;
-    static constexpr int Q = S + D + 2;                // tile metadata slots
-    static constexpr int QT = D + 1;                   // tiles parked in TMEM per warp
+    static constexpr int Q = QT + S + 2;               // tile metadata slots
     static constexpr int WCOLS = 4 * VPT;              // TMEM columns per warp per tile
-    static constexpr int TCOLS = (NC / 4) * WCOLS;     // TMEM columns per tile
-    static_assert(D >= 1 && S >= 2, "need lookahead and a double-buffered ring");
-    static_assert(NC % 4 == 0, "compute warps cover the four TMEM lane quarters evenly");
+    static constexpr int TCOLS = (NR / 4) * WCOLS;     // TMEM columns per tile
+    static constexpr int HALF = (VPT + 1) / 2;         // scan warps: vectors per register pass
+    static_assert(QT >= 2 && S >= 2, "need TMEM slack and a double-buffered ring");
+    static_assert(NR % 4 == 0, "warp groups cover the four TMEM lane quarters evenly");
     static_assert(QT * TCOLS <= 512, "parked tiles must fit the 512 TMEM columns");
+    static_assert(NLB >= 1 && NLB <= S + 1, "sentinel fan-out reuses only retired slots");
 };
 
 constexpr uint64_t kScanSentinel = ~0ull;              // "no more tiles" tag
+
+#ifdef DESC_SCAN_TRACE        // diagnostics builds only: per-tile globaltimer stamps
+constexpr int kTraceTiles = 1 << 16;
+// 0 claim, 1 bytes landed (reduce warp 0), 2 A published, 3 look-back start, 4 look-back end,
+// 5 polls, 6 scan start (prefix in hand), 7 scan end
+__device__ uint64_t g_scan_trace[8][kTraceTiles];
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SCAN_TRACE(f, t, v) do { if ((uint64_t)(t) < (uint64_t)kTraceTiles) g_scan_trace[f][t] = (v); } while (0)
+#else
+#define SCAN_TRACE(f, t, v) do { } while (0)
+#endif
 
 #ifndef DESC_SCAN_DIAG        // diagnostics builds only (wrong results): 1 = no look-back,
 #define DESC_SCAN_DIAG 0      // 2 = outputs are the inputs (no scan arithmetic)
 #endif
 
-template <typename In, int NC, int VPT, int S, int D>
-__global__ void __launch_bounds__(ScanStreamCfg<NC, VPT, S, D>::THREADS, 1)
+template <typename In, int NR, int VPT, int S, int QT, int NLB>
+__global__ void __launch_bounds__(ScanStreamCfg<NR, VPT, S, QT, NLB>::THREADS, 1)
 scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, int64_t ntiles,
                    ScanState<typename AccOf<In>::T> st) {
     using Acc = typename AccOf<In>::T;
-    using C = ScanStreamCfg<NC, VPT, S, D>;
+    using C = ScanStreamCfg<NR, VPT, S, QT, NLB>;
     constexpr int V = 16 / sizeof(In);              // elements per 16-byte vector
     constexpr int TB = C::TB;
     constexpr int Q = C::Q;
     constexpr int64_t T = TB / sizeof(In);          // tile elements
     constexpr int CHUNK = 16384;                    // bytes per bulk copy
+    constexpr int PROD = 2 * NR, AGGR = 2 * NR + 1, LB0 = 2 * NR + 2;   // warp roles
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t full[S], empty[S];          // data ring
     __shared__ __align__(8) uint64_t tag[S];                     // tile id of each ring item
+    __shared__ __align__(8) uint64_t parked[QT], freed[QT];      // TMEM slots
     __shared__ __align__(8) uint64_t wsum[Q], aggb[Q], pfx[Q];   // per tile slot
-    __shared__ __align__(8) uint64_t wtot[Q][NC + 1];            // warp totals + tile id
+    __shared__ __align__(8) uint64_t wtot[Q][NR + 1];            // warp totals + tile id
     __shared__ __align__(8) uint64_t tagg[Q][2];                 // aggregate, tile id
     __shared__ __align__(8) uint64_t tpre[Q];                    // exclusive prefix
     __shared__ uint32_t tmem_base;
@@ -565,7 +597,12 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(ptx::smem_u32(&full[s]), 1);
-            ptx::mbar_init(ptx::smem_u32(&empty[s]), NC);
+            ptx::mbar_init(ptx::smem_u32(&empty[s]), NR);
+        }
+#pragma unroll
+        for (int i = 0; i < QT; ++i) {
+            ptx::mbar_init(ptx::smem_u32(&parked[i]), NR);
+            ptx::mbar_init(ptx::smem_u32(&freed[i]), NR);
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -580,7 +617,7 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
     __syncthreads();
     ptx::tmem_fence_after_sync();
 
-    if (warp == NC) {
+    if (warp == PROD) {
         // ------------------------------------------------------------------ producer
         if (lane != 0) return;
         const uint64_t pol = ptx::policy_evict_first();
@@ -597,6 +634,7 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
                 ptx::st_async_b64(ptx::smem_u32(&tag[s]), kScanSentinel, fb);
                 return;
             }
+            SCAN_TRACE(0, t, gtimer());
             const int64_t rem = nbytes - t * (int64_t)TB;
             const uint32_t bytes = (uint32_t)(rem >= TB ? TB : (rem & ~(int64_t)15));
             ptx::mbar_arrive_expect_tx(fb, bytes + 8);
@@ -608,32 +646,37 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
         }
     }
 
-    if (warp == NC + 1) {
+    if (warp == AGGR) {
         // ------------------------------------------------------------------ aggregator
         for (int64_t k = 0;; ++k) {
             const int q = (int)(k % Q);
             const uint32_t ph = (uint32_t)(k / Q) & 1u;
             const uint32_t wb = ptx::smem_u32(&wsum[q]);
-            if (lane == 0) ptx::mbar_arrive_expect_tx(wb, (NC + 1) * 8);
+            if (lane == 0) ptx::mbar_arrive_expect_tx(wb, (NR + 1) * 8);
             ptx::mbar_wait(wb, ph);
-            const uint64_t tg = wtot[q][NC];
+            const uint64_t tg = wtot[q][NR];
             Acc agg = 0;
 #pragma unroll
-            for (int w = 0; w < NC; ++w) agg += acc_from_bits<Acc>(wtot[q][w]);
+            for (int w = 0; w < NR; ++w) agg += acc_from_bits<Acc>(wtot[q][w]);
             if (lane == 0) {
                 if (tg != kScanSentinel) publish(st, (int64_t)tg, agg, tg == 0 ? 2u : 1u);
-                const uint32_t ab = ptx::smem_u32(&aggb[q]);
-                ptx::mbar_arrive_expect_tx(ab, 16);
-                ptx::st_async_b64(ptx::smem_u32(&tagg[q][0]), acc_bits(agg), ab);
-                ptx::st_async_b64(ptx::smem_u32(&tagg[q][1]), tg, ab);
+                if (tg != kScanSentinel) SCAN_TRACE(2, tg, gtimer());
+                // the sentinel goes to the next NLB slots: one per look-back warp
+                for (int i = 0; i < (tg == kScanSentinel ? NLB : 1); ++i) {
+                    const int qi = (int)((k + i) % Q);
+                    const uint32_t ab = ptx::smem_u32(&aggb[qi]);
+                    ptx::mbar_arrive_expect_tx(ab, 16);
+                    ptx::st_async_b64(ptx::smem_u32(&tagg[qi][0]), acc_bits(agg), ab);
+                    ptx::st_async_b64(ptx::smem_u32(&tagg[qi][1]), tg, ab);
+                }
             }
             if (tg == kScanSentinel) return;
         }
     }
 
-    if (warp == NC + 2) {
+    if (warp >= LB0) {
         // ------------------------------------------------------------------ look-back
-        for (int64_t k = 0;; ++k) {
+        for (int64_t k = warp - LB0;; k += NLB) {
             const int q = (int)(k % Q);
             const uint32_t ph = (uint32_t)(k / Q) & 1u;
             ptx::mbar_wait(ptx::smem_u32(&aggb[q]), ph);
@@ -644,7 +687,14 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
             Acc prefix = 0;
 #if !(DESC_SCAN_DIAG & 1)
             if (t > 0) {
+#ifdef DESC_SCAN_TRACE
+                int polls = 0;
+                if (lane == 0) SCAN_TRACE(3, t, gtimer());
+                prefix = look_back<Acc, 8>(st, t, lane, &polls);
+                if (lane == 0) { SCAN_TRACE(4, t, gtimer()); SCAN_TRACE(5, t, polls); }
+#else
                 prefix = look_back<Acc, 8>(st, t, lane);
+#endif
                 if (lane == 0) publish(st, t, prefix + agg, 2u);
             }
 #endif
@@ -656,104 +706,141 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
         }
     }
 
-    // ---------------------------------------------------------------------- compute warps
-    const uint64_t drop = ptx::policy_evict_first();
-    // this warp's TMEM: lane quarter warp % 4, column block (warp / 4) * WCOLS of each slot
-    const uint32_t tmem_w = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) +
-                            (uint32_t)((warp >> 2) * C::WCOLS);
-    int64_t K = -1;                                      // tiles this CTA got, once known
-    for (int64_t k = 0;; ++k) {
-        if (K < 0) {
-            // R(k): warp total of tile k; its vectors parked in TMEM slot k % QT
+    // segment r of a tile: vectors [r*32*VPT, (r+1)*32*VPT), round v = vectors r*32*VPT +
+    // v*32 + lane; TMEM: lane quarter r % 4, column block (r / 4) * WCOLS of each slot
+    const int r = warp < NR ? warp : warp - NR;
+    const uint32_t tmem_w = tmem_base + ((uint32_t)(32 * (r & 3)) << 16) +
+                            (uint32_t)((r >> 2) * C::WCOLS);
+    if (warp < NR) {
+        // ------------------------------------------------------------------ reduce warps
+        for (int64_t k = 0;; ++k) {
             const int s = (int)(k % S);
             const uint32_t ph = (uint32_t)(k / S) & 1u;
+            const int q = (int)(k % Q);
+            const int qt = (int)(k % QT);
             ptx::mbar_wait(ptx::smem_u32(&full[s]), ph);
             const uint64_t tg = tag[s];
-            const int q = (int)(k % Q);
             Acc wsum_v = 0;
+            uint4 x[VPT];
             if (tg != kScanSentinel) {
+                if (r == 0 && lane == 0) SCAN_TRACE(1, tg, gtimer());
                 const int64_t tbase = (int64_t)tg * T;
                 const uint32_t sbase = ptx::smem_u32(smem + (size_t)s * TB);
-                const uint32_t tm = tmem_w + (uint32_t)((k % C::QT) * C::TCOLS);
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
-                    const int vi = (warp * VPT + v) * 32 + lane;
+                    const int vi = (r * VPT + v) * 32 + lane;
                     const int64_t e0 = tbase + (int64_t)vi * V;
-                    uint4 r;
                     if (e0 + V <= n) {
-                        r = ptx::lds128(sbase + vi * 16);
+                        x[v] = ptx::lds128(sbase + vi * 16);
                     } else {                             // ragged tail: not bulk-copied
-                        r = make_uint4(0, 0, 0, 0);
+                        x[v] = make_uint4(0, 0, 0, 0);
 #pragma unroll
                         for (int e = 0; e < V; ++e)
-                            if (e0 + e < n) set_elem<In>(r, e, in[e0 + e]);
+                            if (e0 + e < n) set_elem<In>(x[v], e, in[e0 + e]);
                     }
-                    wsum_v += vec_sum<In, Acc>(r);
-                    ptx::tmem_st4(tm + 4 * v, r);
+                    wsum_v += vec_sum<In, Acc>(x[v]);
                 }
                 wsum_v = warp_sum(wsum_v);
-            } else {
-                K = k;
+            }
+            // the warp total goes out before the TMEM slot is awaited: a tile's aggregate
+            // depends on nothing but its bytes
+            if (lane == 0) {
+                const uint32_t wb = ptx::smem_u32(&wsum[q]);
+                ptx::st_async_b64(ptx::smem_u32(&wtot[q][r]), acc_bits(wsum_v), wb);
+                if (r == 0) ptx::st_async_b64(ptx::smem_u32(&wtot[q][NR]), tg, wb);
+            }
+            if (tg != kScanSentinel) {
+                ptx::mbar_wait(ptx::smem_u32(&freed[qt]), ((uint32_t)(k / QT) & 1u) ^ 1u);
+                ptx::tmem_fence_after_sync();
+                const uint32_t tm = tmem_w + (uint32_t)(qt * C::TCOLS);
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) ptx::tmem_st4(tm + 4 * v, x[v]);
+                ptx::tmem_wait_st();
+                ptx::tmem_fence_before_sync();
             }
             __syncwarp();
             if (lane == 0) {
                 ptx::mbar_arrive(ptx::smem_u32(&empty[s]));             // stage reusable
-                const uint32_t wb = ptx::smem_u32(&wsum[q]);
-                ptx::st_async_b64(ptx::smem_u32(&wtot[q][warp]), acc_bits(wsum_v), wb);
-                if (warp == 0) ptx::st_async_b64(ptx::smem_u32(&wtot[q][NC]), tg, wb);
+                if (tg != kScanSentinel) ptx::mbar_arrive(ptx::smem_u32(&parked[qt]));
             }
+            if (tg == kScanSentinel) break;
         }
-        const int64_t j = k - D;
-        if (j < 0) continue;
-        if (K >= 0 && j >= K) break;
-        // S(j): scan tile j from its exclusive prefix, vectors back from TMEM
-        const int q = (int)(j % Q);
-        const uint32_t qph = (uint32_t)(j / Q) & 1u;
-        ptx::mbar_wait(ptx::smem_u32(&wsum[q]), qph);    // warp totals (completed phase)
-        ptx::mbar_wait(ptx::smem_u32(&pfx[q]), qph);
-        const int64_t tbase = (int64_t)wtot[q][NC] * T;
-        Acc rcarry = acc_from_bits<Acc>(tpre[q]);
+    } else if (warp < 2 * NR) {
+        // ------------------------------------------------------------------ scan warps
+        const uint64_t drop = ptx::policy_evict_first();
+        for (int64_t j = 0;; ++j) {
+            const int q = (int)(j % Q);
+            const uint32_t qph = (uint32_t)(j / Q) & 1u;
+            const int qt = (int)(j % QT);
+            ptx::mbar_wait(ptx::smem_u32(&wsum[q]), qph);   // warp totals + tile id
+            const uint64_t tg = wtot[q][NR];
+            if (tg == kScanSentinel) break;
+            ptx::mbar_wait(ptx::smem_u32(&pfx[q]), qph);
+            if (r == 0 && lane == 0) SCAN_TRACE(6, tg, gtimer());
+            const int64_t tbase = (int64_t)tg * T;
+            Acc rcarry = acc_from_bits<Acc>(tpre[q]);
 #pragma unroll
-        for (int w = 0; w < NC; ++w)
-            if (w < warp) rcarry += acc_from_bits<Acc>(wtot[q][w]);
-        ptx::tmem_wait_st();                             // R's parking stores complete
-        const uint32_t tm = tmem_w + (uint32_t)((j % C::QT) * C::TCOLS);
-        uint4 raw[VPT];
+            for (int w = 0; w < NR; ++w)
+                if (w < r) rcarry += acc_from_bits<Acc>(wtot[q][w]);
+            ptx::mbar_wait(ptx::smem_u32(&parked[qt]), (uint32_t)(j / QT) & 1u);
+            ptx::tmem_fence_after_sync();
+            const uint32_t tm = tmem_w + (uint32_t)(qt * C::TCOLS);
 #pragma unroll
-        for (int v = 0; v < VPT; ++v) raw[v] = ptx::tmem_ld4(tm + 4 * v);
-        ptx::tmem_wait_ld();
+            for (int h = 0; h < VPT; h += C::HALF) {
+                constexpr int H = C::HALF;
+                uint4 x[H];
 #pragma unroll
-        for (int v = 0; v < VPT; ++v)                    // registers valid only after the wait
-            asm volatile("" : "+r"(raw[v].x), "+r"(raw[v].y), "+r"(raw[v].z), "+r"(raw[v].w));
+                for (int v = 0; v < H; ++v)
+                    if (h + v < VPT) x[v] = ptx::tmem_ld4(tm + 4 * (h + v));
+                ptx::tmem_wait_ld();
 #pragma unroll
-        for (int v = 0; v < VPT; ++v) {
-            const int vi = (warp * VPT + v) * 32 + lane;
-            const int64_t e0 = tbase + (int64_t)vi * V;
-            const Acc ls = vec_sum<In, Acc>(raw[v]);
-            const Acc wi = warp_incl_scan(ls, lane);
-            Acc run = rcarry + warp_excl_from_incl(wi, lane);
-            rcarry += __shfl_sync(0xffffffffu, wi, 31);
-            uint4 o = make_uint4(0, 0, 0, 0);
+                for (int v = 0; v < H; ++v)              // registers valid only after the wait
+                    asm volatile("" : "+r"(x[v].x), "+r"(x[v].y), "+r"(x[v].z), "+r"(x[v].w));
+                if (h + H >= VPT) {                      // last pass: the slot can be reused
+                    ptx::tmem_fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&freed[qt]));
+                }
+                // the rounds' warp scans are independent: run them level by level together
+                Acc wi[H], wex[H], wt[H];
 #pragma unroll
-            for (int e = 0; e < V; ++e) {
-                run += to_acc<Acc>(unpack<In>(raw[v], e));
-                set_elem<In>(o, e, (In)run);
-            }
+                for (int v = 0; v < H; ++v) wi[v] = h + v < VPT ? vec_sum<In, Acc>(x[v]) : Acc(0);
+                warp_incl_scan_n<Acc, H>(wi, lane);
+#pragma unroll
+                for (int v = 0; v < H; ++v) {
+                    wex[v] = warp_excl_from_incl(wi[v], lane);
+                    wt[v] = __shfl_sync(0xffffffffu, wi[v], 31);
+                }
+#pragma unroll
+                for (int v = 0; v < H; ++v) {
+                    if (h + v >= VPT) break;
+                    const int vi = (r * VPT + h + v) * 32 + lane;
+                    const int64_t e0 = tbase + (int64_t)vi * V;
+                    Acc run = rcarry + wex[v];
+                    rcarry += wt[v];
+                    uint4 o = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        run += to_acc<Acc>(unpack<In>(x[v], e));
+                        set_elem<In>(o, e, (In)run);
+                    }
 #if DESC_SCAN_DIAG & 2
-            o = raw[v];
+                    o = x[v];
 #endif
-            if (e0 + V <= n) {
-                ptx::stg128_hint(out + e0, o, drop);
-            } else {
+                    if (e0 + V <= n) {
+                        ptx::stg128_hint(out + e0, o, drop);
+                    } else {
 #pragma unroll
-                for (int e = 0; e < V; ++e)
-                    if (e0 + e < n) out[e0 + e] = unpack<In>(o, e);
+                        for (int e = 0; e < V; ++e)
+                            if (e0 + e < n) out[e0 + e] = unpack<In>(o, e);
+                    }
+                }
             }
         }
     }
-    // release TMEM: every compute warp is done with its columns
+    // release TMEM once both warp groups are done with it
     ptx::tmem_fence_before_sync();
-    ptx::named_bar_sync(1, 32 * NC);
+    ptx::named_bar_sync(1, 32 * 2 * NR);
     if (warp == 0) {
         ptx::tmem_fence_after_sync();
         ptx::tmem_dealloc(tmem_base, 512);

@@ -5,12 +5,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2305_03448_b200 import build as B
 
 VARIANTS = {
+    "lb2": ["DESC_SCAN_LB_WARPS=2"],
+    "qt4": ["DESC_SCAN_TMEM_SLOTS=4"],
+    "v10": ["DESC_SCAN_VPT=10"],
+    "v16s3q4": ["DESC_SCAN_VPT=16", "DESC_SCAN_STAGES=3", "DESC_SCAN_TMEM_SLOTS=4"],
     "diag1": ["DESC_SCAN_DIAG=1"],
     "diag3": ["DESC_SCAN_DIAG=3"],
-    "d3": ["DESC_SCAN_LOOKAHEAD=3"],
-    "s3": ["DESC_SCAN_STAGES=3"],
-    "v4d6": ["DESC_SCAN_VPT=4", "DESC_SCAN_LOOKAHEAD=6", "DESC_SCAN_STAGES=6"],
-    "v5d5": ["DESC_SCAN_VPT=5", "DESC_SCAN_LOOKAHEAD=5", "DESC_SCAN_STAGES=5"],
 }
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)

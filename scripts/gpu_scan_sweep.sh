@@ -6,7 +6,7 @@ y=d.scan(x, algo='stream'); torch.cuda.synchronize(); print('stream quick', (x.l
 " 2>&1 | tail -2
 timeout 900 python -m pytest tests/test_reduce_scan_gpu.py -x -q > gpurun_out/pytest_scan.log 2>&1; echo pytest rc=$?
 tail -3 gpurun_out/pytest_scan.log
-for v in base diag1 diag3 d3 s3 v4d6 v5d5; do
+for v in base lb2 qt4 v10 v16s3q4 diag1 diag3; do
   if [ $v = base ]; then L=""; else L=build_variants/lib_$v.so; fi
   for w in scan64M_f32 scan64M_i32; do
     DESC_LIB=$L timeout 300 python bench.py --workload $w --scan-algo stream --no-oracle --steps 300 --warmup 20 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', '$w', d['value'], d['roofline']['frac'])"
