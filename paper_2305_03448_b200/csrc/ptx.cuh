@@ -47,6 +47,18 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t count) {
                  : "memory");
 }
 
+// Non-blocking probe: has the phase with parity `parity` completed?
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0;
+}
+
 // Asynchronous 8-byte store into (this CTA's) shared memory that completes as `bytes` on the
 // mbarrier, like a TMA load: the consumer sees the value after its mbarrier wait.
 __device__ __forceinline__ void st_async_b64(uint32_t addr, uint64_t v, uint32_t bar) {

@@ -153,14 +153,16 @@ block_reduce_cta_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_
 // relaxed gpu-scope 8-byte accesses, which are single-copy atomic: a reader that sees a
 // status also sees its value, so no fence sits on the look-back's critical path (a gpu-scope
 // fence waits for the thread's outstanding stores, microseconds under a full HBM stream).
-// 64-bit values are split over two words (lo, hi) that carry the same status; a reader that
-// sees two different statuses (the A -> P update in between) treats the tile as not ready
-// and polls again.
+// 64-bit values are split over two adjacent words (lo, hi) that carry the same status and
+// move as one 16-byte access; a reader that sees two different statuses (a torn A -> P
+// update) treats the tile as not ready and polls again.
 template <typename Acc>
 struct ScanState {
     uint32_t *counter;   // tile claim counter (64-bit for the streaming scan)
-    uint64_t *dlo;       // single pass: descriptor word {value[31:0], status}
-    uint64_t *dhi;       // single pass, 64-bit values: {value[63:32], status}
+    uint64_t *dlo;       // single pass: descriptor words; 32-bit values: {value, status} at
+                         // [t]; 64-bit values: {value[31:0], status}, {value[63:32], status}
+                         // at [2t], [2t+1] (one 16-byte access each way)
+    uint64_t *dhi;       // unused (kept for the workspace layout)
     Acc *agg;            // three-launch: per-tile aggregate
     Acc *incl;           // three-launch: per-tile exclusive prefix
 };
@@ -173,6 +175,16 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
     uint64_t v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+// 16-byte relaxed accesses: each 8-byte half is single-copy atomic (all the protocol needs:
+// a torn pair shows two different statuses and is read again)
+__device__ __forceinline__ void st_relaxed_v2u64(uint64_t *p, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ void ld_relaxed_v2u64(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
 template <typename Acc>
@@ -204,22 +216,26 @@ template <typename Acc>
 __device__ __forceinline__ void publish(const ScanState<Acc> &st, int64_t t, Acc v,
                                         uint32_t status) {
     const uint64_t b = acc_bits(v);
-    st_relaxed_u64(&st.dlo[t], (b << 32) | status);
-    if constexpr (sizeof(Acc) == 8) st_relaxed_u64(&st.dhi[t], (b & 0xFFFFFFFF00000000ull) | status);
+    if constexpr (sizeof(Acc) == 8)
+        st_relaxed_v2u64(&st.dlo[2 * t], (b << 32) | status, (b & 0xFFFFFFFF00000000ull) | status);
+    else
+        st_relaxed_u64(&st.dlo[t], (b << 32) | status);
 }
 
 // status of tile t (0 while not ready or torn between A and P) and its value
 template <typename Acc>
 __device__ __forceinline__ uint32_t read_desc(const ScanState<Acc> &st, int64_t t, Acc &v) {
-    const uint64_t lo = ld_relaxed_u64(&st.dlo[t]);
     if constexpr (sizeof(Acc) == 8) {
-        const uint64_t hi = ld_relaxed_u64(&st.dhi[t]);
+        uint64_t lo, hi;
+        ld_relaxed_v2u64(&st.dlo[2 * t], lo, hi);
         if ((uint32_t)lo != (uint32_t)hi) return 0u;
         v = acc_from_bits<Acc>((hi & 0xFFFFFFFF00000000ull) | (lo >> 32));
+        return (uint32_t)lo;
     } else {
+        const uint64_t lo = ld_relaxed_u64(&st.dlo[t]);
         v = acc_from_bits<Acc>(lo >> 32);
+        return (uint32_t)lo;
     }
-    return (uint32_t)lo;
 }
 
 template <typename Acc>
@@ -257,6 +273,10 @@ __device__ __forceinline__ Acc warp_excl_from_incl(Acc incl, int lane) {
 // aggregates (A) of the tiles after it.  Lane l reads descriptors j - 32 m - l (m < LB), so
 // every poll is LB coalesced requests and a window covers 32 * LB predecessors; while a
 // needed predecessor is not ready the warp sleeps briefly and polls again.
+#ifndef DESC_SCAN_SLEEP_CAP   // longest back-off between look-back polls, ns
+#define DESC_SCAN_SLEEP_CAP 256
+#endif
+
 template <typename Acc, int LB>
 __device__ Acc look_back(const ScanState<Acc> &st, int64_t tile, int lane, int *polls = nullptr) {
     constexpr int W = 32 * LB;
@@ -284,7 +304,7 @@ __device__ Acc look_back(const ScanState<Acc> &st, int64_t tile, int lane, int *
             if (m * 32 + lane <= dp && f[m] == 0u) missing = true;
         if (__any_sync(0xffffffffu, missing)) {
             __nanosleep(ns);
-            if (ns < 256) ns <<= 1;
+            if (ns < DESC_SCAN_SLEEP_CAP) ns <<= 1;
             continue;
         }
         Acc sum = 0;

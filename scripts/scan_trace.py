@@ -35,3 +35,5 @@ print("landed -> scan start   ", q(b[6] - b[1]))
 A = b[2]
 lag = np.array([A[max(0, t - 148):t].max() - A[t] for t in range(1, nt)])
 print("max(A of 148 preds) - A(t)", q(lag))
+np_ = (buf[7, :nt] > 0).sum()
+print(f"tiles with a segment re-read from L2: {np_} of {nt}; segments: {int(buf[7, :nt].sum())}")
