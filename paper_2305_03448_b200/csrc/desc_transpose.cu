@@ -1179,7 +1179,17 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
         e = cudaMemsetAsync(work, 0, 256 + desc_words * round_up(ts * 8, 256), stream);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (scan state)");
         const int64_t grid = ts < di.sms ? ts : di.sms;
-        e = launch_cluster2(kern, (int)grid, SC::THREADS, smem, stream, pi, po, n, ts, st);
+        // TMA view of the input: rows of 128 bytes (the < 128-byte tail is read directly)
+        const int64_t bulk_rows = n * es / 128;
+        CUtensorMap map;
+        memset(&map, 0, sizeof(map));
+        if (bulk_rows > 0) {
+            MapKey k{reinterpret_cast<uintptr_t>(in), 128 / es, bulk_rows, 1, 128 / es, 0, es,
+                     128 / es, SC::BOX_ROWS};
+            if (desc_status s = tensor_map(k, &map)) return s;
+        }
+        e = launch_cluster2(kern, (int)grid, SC::THREADS, smem, stream, map, pi, po, n, ts,
+                            bulk_rows, st);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "scan_stream launch");
         g_last_launches = 1;

@@ -273,6 +273,9 @@ __device__ __forceinline__ Acc warp_excl_from_incl(Acc incl, int lane) {
 // aggregates (A) of the tiles after it.  Lane l reads descriptors j - 32 m - l (m < LB), so
 // every poll is LB coalesced requests and a window covers 32 * LB predecessors; while a
 // needed predecessor is not ready the warp sleeps briefly and polls again.
+#ifndef DESC_SCAN_LB_WINDOW   // streaming scan: look-back window, x32 predecessors per poll
+#define DESC_SCAN_LB_WINDOW 1
+#endif
 #ifndef DESC_SCAN_SLEEP_CAP   // longest back-off between look-back polls, ns
 #define DESC_SCAN_SLEEP_CAP 256
 #endif
@@ -558,7 +561,11 @@ template <int NR, int VPT, int S, int QT, int NLB>
 struct ScanStreamCfg {
     static constexpr int THREADS = 32 * (2 * NR + 2 + NLB);
     static constexpr int TB = NR * 32 * VPT * 16;      // tile bytes
-    static constexpr int SMEM = S * TB;
+    static constexpr int ROWS = TB / 128;              // 128-byte rows per tile (TMA view)
+    static constexpr int NBOX = (ROWS + 255) / 256;    // boxes of <= 256 rows per tile
+    static constexpr int BOX_ROWS = ROWS / NBOX;
+    static constexpr int SMEM = S * TB + 1024;         // stages 1024-byte aligned (swizzle)
+    static_assert(ROWS % NBOX == 0, "tile rows must split into equal TMA boxes");
     static constexpr int Q = QT + S + 2;               // tile metadata slots
     static constexpr int WCOLS = 4 * VPT;              // TMEM columns per warp per tile
     static constexpr int TCOLS = (NR / 4) * WCOLS;     // TMEM columns per tile
@@ -592,7 +599,8 @@ __device__ __forceinline__ uint64_t gtimer() {
 
 template <typename In, int NR, int VPT, int S, int QT, int NLB>
 __global__ void __launch_bounds__(ScanStreamCfg<NR, VPT, S, QT, NLB>::THREADS, 1)
-scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, int64_t ntiles,
+scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restrict__ in,
+                   In *__restrict__ out, int64_t n, int64_t ntiles, int64_t bulk_rows,
                    ScanState<typename AccOf<In>::T> st) {
     using Acc = typename AccOf<In>::T;
     using C = ScanStreamCfg<NR, VPT, S, QT, NLB>;
@@ -600,9 +608,13 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
     constexpr int TB = C::TB;
     constexpr int Q = C::Q;
     constexpr int64_t T = TB / sizeof(In);          // tile elements
-    constexpr int CHUNK = 16384;                    // bytes per bulk copy
     constexpr int PROD = 2 * NR, AGGR = 2 * NR + 1, LB0 = 2 * NR + 2;   // warp roles
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    // the input is seen by TMA as rows of 128 bytes (bulk_rows of them; the < 128-byte tail
+    // is read directly), loaded with the 128-byte swizzle: 16-byte chunk c of row w of a
+    // stage sits at chunk c ^ (w & 7), so the warp-striped reads below are conflict-free
+    const uint32_t ring = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    const int64_t n_bulk = bulk_rows * (128 / (int64_t)sizeof(In));
     __shared__ __align__(8) uint64_t full[S], empty[S];          // data ring
     __shared__ __align__(8) uint64_t tag[S];                     // tile id of each ring item
     __shared__ __align__(8) uint64_t parked[QT], freed[QT];      // TMEM slots
@@ -641,7 +653,7 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
         // ------------------------------------------------------------------ producer
         if (lane != 0) return;
         const uint64_t pol = ptx::policy_evict_first();
-        const int64_t nbytes = n * (int64_t)sizeof(In);
+        ptx::prefetch_tensormap(&map_in);
         for (int64_t k = 0;; ++k) {
             const int s = (int)(k % S);
             const uint32_t ph = (uint32_t)(k / S) & 1u;
@@ -655,14 +667,17 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
                 return;
             }
             SCAN_TRACE(0, t, gtimer());
-            const int64_t rem = nbytes - t * (int64_t)TB;
-            const uint32_t bytes = (uint32_t)(rem >= TB ? TB : (rem & ~(int64_t)15));
-            ptx::mbar_arrive_expect_tx(fb, bytes + 8);
+            // boxes that start inside the TMA view (rows past its end are zero-filled and
+            // never read back: the reduce warps take those vectors from global memory)
+            const int64_t row0 = t * C::ROWS;
+            int nb = 0;
+            while (nb < C::NBOX && row0 + (int64_t)nb * C::BOX_ROWS < bulk_rows) ++nb;
+            ptx::mbar_arrive_expect_tx(fb, (uint32_t)(nb * C::BOX_ROWS * 128) + 8);
             ptx::st_async_b64(ptx::smem_u32(&tag[s]), (uint64_t)t, fb);
-            const uint32_t dst = ptx::smem_u32(smem + (size_t)s * TB);
-            const uint8_t *src = reinterpret_cast<const uint8_t *>(in) + t * (int64_t)TB;
-            for (uint32_t c = 0; c < bytes; c += CHUNK)
-                ptx::bulk_load_1d(dst + c, src + c, bytes - c < CHUNK ? bytes - c : CHUNK, fb, pol);
+            const uint32_t dst = ring + (uint32_t)s * TB;
+            for (int b = 0; b < nb; ++b)
+                ptx::tma_load_2d(dst + b * C::BOX_ROWS * 128, &map_in, fb, 0,
+                                 (int32_t)(row0 + (int64_t)b * C::BOX_ROWS), pol);
         }
     }
 
@@ -710,10 +725,10 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
 #ifdef DESC_SCAN_TRACE
                 int polls = 0;
                 if (lane == 0) SCAN_TRACE(3, t, gtimer());
-                prefix = look_back<Acc, 8>(st, t, lane, &polls);
+                prefix = look_back<Acc, DESC_SCAN_LB_WINDOW>(st, t, lane, &polls);
                 if (lane == 0) { SCAN_TRACE(4, t, gtimer()); SCAN_TRACE(5, t, polls); }
 #else
-                prefix = look_back<Acc, 8>(st, t, lane);
+                prefix = look_back<Acc, DESC_SCAN_LB_WINDOW>(st, t, lane);
 #endif
                 if (lane == 0) publish(st, t, prefix + agg, 2u);
             }
@@ -745,14 +760,15 @@ scan_stream_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n, i
             if (tg != kScanSentinel) {
                 if (r == 0 && lane == 0) SCAN_TRACE(1, tg, gtimer());
                 const int64_t tbase = (int64_t)tg * T;
-                const uint32_t sbase = ptx::smem_u32(smem + (size_t)s * TB);
+                const uint32_t sbase = ring + (uint32_t)s * TB;
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
                     const int vi = (r * VPT + v) * 32 + lane;
                     const int64_t e0 = tbase + (int64_t)vi * V;
-                    if (e0 + V <= n) {
-                        x[v] = ptx::lds128(sbase + vi * 16);
-                    } else {                             // ragged tail: not bulk-copied
+                    if (e0 + V <= n_bulk) {
+                        const int w = vi >> 3;
+                        x[v] = ptx::lds128(sbase + w * 128 + (((vi & 7) ^ (w & 7)) << 4));
+                    } else {                             // tail: not in the TMA view
                         x[v] = make_uint4(0, 0, 0, 0);
 #pragma unroll
                         for (int e = 0; e < V; ++e)

@@ -115,11 +115,19 @@ view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const Vie
                     if (uok && rr < r1) *reinterpret_cast<T *>(oitem + (rr * v.U + u) * CB) = c[k];
                 }
             }
-        } else {                              // long rows: consecutive cells per warp
-            for (int64_t r = r0 + tr; r < r1; r += rpp) {
+        } else {                              // long rows: consecutive cells per warp,
+            for (int64_t r = r0 + tr; r < r1; r += rpp) {   // 4 loads in flight per thread
                 const int64_t in_row = obase + r * v.s2;
                 char *orow = oitem + r * v.U * CB;
-                for (int64_t u = u0 + tu; u < u1; u += uw)
+                int64_t u = u0 + tu;
+                for (; u + 3 * uw < u1; u += 4 * uw) {
+                    T c[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) c[k] = IO::load(in, in_row, u + k * uw, v.s1, es);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) *reinterpret_cast<T *>(orow + (u + k * uw) * CB) = c[k];
+                }
+                for (; u < u1; u += uw)
                     *reinterpret_cast<T *>(orow + u * CB) = IO::load(in, in_row, u, v.s1, es);
             }
         }
