@@ -623,11 +623,34 @@ desc_status dispatch(const Args &a, desc_kernel k) {
     return fail(DESC_ERR_KERNEL, "unknown kernel variant %d", (int)k);
 }
 
+// Test-teeth variant (-DDESC_MUTANTS, mutants.cuh): DESC_MUTANT=<id> selects one defect; the
+// id is copied to the device once per device.  The product build has no such state.
+#ifdef DESC_MUTANTS
+int host_mutant() {
+    static const int id = [] { const char *e = getenv("DESC_MUTANT"); return e ? atoi(e) : 0; }();
+    static bool synced[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev < 64 && !synced[dev]) {
+        cudaMemcpyToSymbol(desc::g_desc_mutant, &id, sizeof id);
+        synced[dev] = true;
+    }
+    return id;
+}
+#else
+constexpr int host_mutant() { return 0; }
+#endif
+
 desc_status run(const Args &a, desc_kernel k) {
     g_last_launches = 0;
     bool empty;
     if (desc_status s = validate(a, &empty)) return s;
     if (empty) return DESC_OK;
+    if (host_mutant() == desc::MUT_SWAP_LD) {
+        Args b = a;
+        b.ld_in = a.ld_out;
+        b.ld_out = a.ld_in;
+        return dispatch(b, k);
+    }
     return dispatch(a, k);
 }
 
@@ -1060,6 +1083,7 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
 desc_status run_reduce(const void *in, void *out, int64_t n, int64_t B, desc_dtype dtype,
                        cudaStream_t stream) {
     g_last_launches = 0;
+    host_mutant();
     const int es = rs_es(dtype);
     if (es == 0) return fail(DESC_ERR_DTYPE, "block reduction supports u8, i32, i64, f32, f64");
     if (n < 0 || B <= 0) return fail(DESC_ERR_SHAPE, "need n >= 0 and block > 0");
@@ -1220,6 +1244,7 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
 desc_status run_scan(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
                      size_t work_bytes, desc_scan_algo algo, cudaStream_t stream) {
     g_last_launches = 0;
+    host_mutant();
     const int es = rs_es(dtype);
     if (es == 0) return fail(DESC_ERR_DTYPE, "scan supports u8, i32, i64, f32, f64");
     if (n < 0) return fail(DESC_ERR_SHAPE, "negative n");

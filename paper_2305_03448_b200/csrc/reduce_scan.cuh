@@ -25,6 +25,7 @@
 #include <cstring>
 #include <type_traits>
 
+#include "mutants.cuh"
 #include "ptx.cuh"
 
 namespace desc {
@@ -105,6 +106,7 @@ __device__ __forceinline__ Acc range_sum(const In *__restrict__ in, int64_t lo, 
                vec_sum<In, Acc>(v3);
     }
     for (; k < nv; k += nl) acc += vec_sum<In, Acc>(ld_nc_v4(vp + k));
+    if (DESC_MUTANT(MUT_REDUCE_NO_TAIL)) return acc;
     for (int64_t i = a + nv * V + lane; i < hi; i += nl) acc += to_acc<Acc>(in[i]);
     return acc;
 }
@@ -395,7 +397,8 @@ scan_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
             if (lane == 0) publish(st, 0, agg, 2u);
         } else {
             if (lane == 0) publish(st, tile, agg, 1u);
-            prefix = look_back<Acc, 4>(st, tile, lane);      // 4: no spills at 64 registers
+            if (!DESC_MUTANT(MUT_SCAN_NO_LOOKBACK))
+                prefix = look_back<Acc, 4>(st, tile, lane);  // 4: no spills at 64 registers
             if (lane == 0) publish(st, tile, prefix + agg, 2u);
         }
         if (lane == 0) tile_prefix = prefix;
@@ -499,7 +502,7 @@ scan_tiles_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n,
     for (int k = 0; k < R; ++k) carry += warp_sum(vec_sum<In, Acc>(raw[k]));
     if (lane == 0) warp_tot[warp] = carry;
     __syncthreads();
-    Acc wpre = excl[tile];
+    Acc wpre = DESC_MUTANT(MUT_SCAN_NO_LOOKBACK) ? Acc(0) : excl[tile];
 #pragma unroll
     for (int w = 0; w < 8; ++w)
         if (w < warp) wpre += warp_tot[w];
@@ -721,7 +724,7 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
             const Acc agg = acc_from_bits<Acc>(tagg[q][0]);
             Acc prefix = 0;
 #if !(DESC_SCAN_DIAG & 1)
-            if (t > 0) {
+            if (t > 0 && !DESC_MUTANT(MUT_SCAN_NO_LOOKBACK)) {
 #ifdef DESC_SCAN_TRACE
                 int polls = 0;
                 if (lane == 0) SCAN_TRACE(3, t, gtimer());

@@ -11,6 +11,8 @@
 #pragma once
 #include <cstdint>
 
+#include "mutants.cuh"
+
 namespace desc {
 
 template <typename Cell>
@@ -31,13 +33,24 @@ transpose_smem_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int64
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {                 // copy-in, P:52-55 (fixed)
             const int64_t i = ti * 32 + ty + j, c = tj * 32 + tx;
-            if (i < rows && c < cols) tile[ty + j][tx] = src[i * ld_in + c];
+            if (i < rows && c < cols) {
+                Cell v = src[i * ld_in + c];
+                if constexpr (sizeof(Cell) == 8) {             // test-teeth variant only
+                    if (DESC_MUTANT(MUT_SMEM_FLOAT_TMP))
+                        v = (Cell)__double_as_longlong((double)(float)__longlong_as_double((long long)v));
+                }
+                if (DESC_MUTANT(MUT_SMEM_NO_PAREN)) (&tile[0][0])[ty + j * 33 + tx] = v;
+                else tile[ty + j][tx] = v;
+            }
         }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {                 // copy-out
             const int64_t orow = tj * 32 + ty + j, ocol = ti * 32 + tx;
-            if (orow < cols && ocol < rows) dst[orow * ld_out + ocol] = tile[tx][ty + j];
+            const int64_t ocol_lim = rows + (DESC_MUTANT(MUT_SMEM_EDGE) ? 1 : 0);
+            if (orow < cols && ocol < ocol_lim)
+                dst[orow * ld_out + ocol] = DESC_MUTANT(MUT_SMEM_TILE_ONLY) ? tile[ty + j][tx]
+                                                                           : tile[tx][ty + j];
         }
         __syncthreads();                                  // tile reused by the next iteration
     }

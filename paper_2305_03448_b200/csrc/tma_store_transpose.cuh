@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <cuda.h>
 
+#include "mutants.cuh"
 #include "ptx.cuh"
 #include "tma_transpose.cuh"
 
@@ -200,8 +201,9 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
                 // logical row row0+k lives in physical box row TR-1-(row0+k) when reversed;
                 // (TR-1-x) & 7 == 7 ^ (x & 7), so the phase stays conflict-free
                 const int row = p.rev_rows ? TR - 1 - (row0 + k) : row0 + k;
+                const int sw = DESC_MUTANT(MUT_TMA2_NO_SWIZZLE) ? 0 : (row & 7);
                 r[q][k] = ptx::lds128(sbase + task_box(q) * C::BOX_BYTES + row * 128 +
-                                      ((task_chunk(q) ^ (row & 7)) << 4));
+                                      ((task_chunk(q) ^ sw) << 4));
             }
         }
         __syncwarp();
@@ -218,6 +220,10 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
                 uint4 o0 = rotated_row<4, 0>(r[q], flip), o1 = rotated_row<4, 1>(r[q], flip);
                 uint4 o2 = rotated_row<4, 2>(r[q], flip), o3 = rotated_row<4, 3>(r[q], flip);
                 const int f = flip;
+                if (DESC_MUTANT(MUT_TMA2_NO_MICRO)) {           // chunks stored untransposed
+                    o0 = f ? r[q][2] : r[q][0]; o1 = f ? r[q][3] : r[q][1];
+                    o2 = f ? r[q][0] : r[q][2]; o3 = f ? r[q][1] : r[q][3];
+                }
                 int row;
                 row = orow0 + (0 ^ f); ptx::sts128(ob + row * 128 + ((c ^ (row & 7)) << 4), o0);
                 row = orow0 + (1 ^ f); ptx::sts128(ob + row * 128 + ((c ^ (row & 7)) << 4), o1);
@@ -226,6 +232,7 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
             } else {
                 uint4 o0 = rotated_row<8, 0>(r[q], flip), o1 = rotated_row<8, 1>(r[q], flip);
                 const int f = flip;
+                if (DESC_MUTANT(MUT_TMA2_NO_MICRO)) { o0 = f ? r[q][1] : r[q][0]; o1 = f ? r[q][0] : r[q][1]; }
                 int row;
                 row = orow0 + (0 ^ f); ptx::sts128(ob + row * 128 + ((c ^ (row & 7)) << 4), o0);
                 row = orow0 + (1 ^ f); ptx::sts128(ob + row * 128 + ((c ^ (row & 7)) << 4), o1);
@@ -234,7 +241,7 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
         // Ragged tail (rows % VEC != 0): TMA stores clip only at 16-byte granularity, so the
         // output tensor map stops at rows_main = rows rounded down to VEC and the lanes whose
         // micro-block straddles `rows` write the remaining columns themselves (R6, R8).
-        if (p.rows_main != p.rows) {
+        if (p.rows_main != p.rows && !DESC_MUTANT(MUT_TMA2_NO_TAIL)) {
             const TileCoord tc = tile_coords(t, p);
 #pragma unroll
             for (int q = 0; q < TPW; ++q) {
@@ -248,8 +255,10 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
                 }
             }
         }
-        ptx::fence_proxy_async_shared();                 // generic writes -> async proxy
-        if (issuer) ptx::bulk_wait_group_read<OBUF - 2>();   // buffer (it+1)%OBUF reusable
+        if (!DESC_MUTANT(MUT_TMA2_NO_FENCE)) {
+            ptx::fence_proxy_async_shared();             // generic writes -> async proxy
+            if (issuer) ptx::bulk_wait_group_read<OBUF - 2>();   // buffer (it+1)%OBUF reusable
+        }
         ptx::named_bar_sync(1, 32 * CW);
         if (issuer) {
             const TileCoord tc = tile_coords(t, p);

@@ -62,6 +62,12 @@ def test_sass_is_sm100a_with_tma(lib):
         assert "UTMASTG" in blk, "TMA-store kernel does not issue bulk tensor stores"
 
 
+def test_product_build_carries_no_test_defects(lib):
+    """The test-teeth defects (csrc/mutants.cuh) exist only in the -DDESC_MUTANTS variant."""
+    with open(desc.lib_path, "rb") as f:
+        assert b"g_desc_mutant" not in f.read()
+
+
 def test_host_helpers(lib):
     assert desc.desc_version() >= 100
     assert desc.desc_dtype_size("f32") == 4 and desc.desc_dtype_size("f64") == 8
