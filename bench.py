@@ -300,6 +300,51 @@ def reference_arm(args, wl, world, rank):
 
 
 # ------------------------------------------------------------------------- our arm
+def small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush, per_launch,
+                          step_bytes, reps: int = 100):
+    """Context for L2-flushed (small) workloads, outside the timed region: (1) the launch
+    floor -- the same kernel on a one-tile problem of the same dtype, timed the same way
+    (flush, events around the launch), i.e. launch + prologue + one load/store round trip;
+    (2) the same launches back to back without a flush (L2-resident, not the metric)."""
+    tdt = {"f32": torch.float32, "f64": torch.float64, "i32": torch.int32}[wl["dtype"]]
+    tr = 64 if wl["es"] == 8 else 128
+    xt = torch.zeros((tr, 128 // wl["es"]), dtype=tdt, device=dev)
+    yt = torch.empty((128 // wl["es"], tr), dtype=tdt, device=dev)
+    sptr = stream.cuda_stream
+
+    def tiny():
+        desc.desc_transpose_ex(xt.data_ptr(), yt.data_ptr(), 1, xt.shape[0], xt.shape[1],
+                               xt.shape[1], xt.shape[0], 0, 0, wl["dtype"], kernel, sptr)
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+    for k in range(reps):
+        l2_flush()
+        ev[2 * k].record(stream)
+        tiny()
+        ev[2 * k + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    floor = statistics.median(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(reps))
+    med = statistics.median(per_launch)
+    warm0, warm1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(5):
+        step()
+    warm0.record(stream)
+    for _ in range(reps):
+        step()
+    warm1.record(stream)
+    torch.cuda.synchronize(dev)
+    warm_ms = warm0.elapsed_time(warm1) / reps
+    return {"launch_floor_ms": round(floor, 5),
+            "launch_floor_what": f"same kernel, one {tuple(xt.shape)} tile, flushed L2, "
+                                 "events around the launch (median of 100); an empty torch "
+                                 "kernel timed this way takes ~6.2 us on B200 "
+                                 "(profiles/r01_exp_floor.txt)",
+            "launch_median_ms": round(med, 5),
+            "l2_resident_gbs": round(step_bytes / (warm_ms / 1e3) / 1e9, 1),
+            "l2_resident_what": "the same launches back to back, no flush (working set in "
+                                "the 126 MB L2; context, not the metric)"}
+
+
 def ours_arm(args, wl, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -409,6 +454,8 @@ def ours_arm(args, wl, world, rank, local):
         torch.cuda.synchronize(dev)
         per_launch = [ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(n_diag)]
     peak, peak_src = load_peak()
+    small = small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush,
+                                  per_launch, step_bytes) if flush else None
 
     # ---- parity of the timed output (rank-local) ------------------------------------
     parity = None
@@ -463,6 +510,7 @@ def ours_arm(args, wl, world, rank, local):
             "e2e": e2e,
             "parity": parity,
             "gpu_launches": launches,
+            **({"small_problem": small} if small else {}),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -751,6 +799,33 @@ def op_arm(args, wl, world, rank, local):
     return 0
 
 
+def pcie_ceiling(torch, dev, h_in, h_out, reps: int = 3) -> float:
+    """GB/s (H2D + D2H bytes) of a plain pinned H2D copy of h_in concurrent with a plain D2H
+    copy into h_out on two streams, per rank -- the PCIe bound of the e2e measurement."""
+    d_a = torch.empty(h_in.numel(), dtype=h_in.dtype, device=dev)
+    d_b = torch.empty(h_out.numel(), dtype=h_out.dtype, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    hi, ho = h_in.reshape(-1), h_out.reshape(-1)
+    best = 0.0
+    for _ in range(reps):
+        torch.cuda.synchronize(dev)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(s1)
+        s2.wait_event(e0)
+        with torch.cuda.stream(s1):
+            d_a.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(s2):
+            ho.copy_(d_b, non_blocking=True)
+        e1.record(s1)
+        e2.record(s2)
+        torch.cuda.synchronize(dev)
+        ms = max(e0.elapsed_time(e1), e0.elapsed_time(e2))
+        best = max(best, (hi.numel() * hi.element_size() + ho.numel() * ho.element_size())
+                   / (ms / 1e3) / 1e9)
+    del d_a, d_b
+    return best
+
+
 def measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, wl, kernel, world):
     """Same metric end to end through the public host-buffer API desc_transpose_host:
     pinned host input -> (H2D band k+1 | transpose band k | D2H band k-1, pipelined on two
@@ -783,7 +858,14 @@ def measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, w
     torch.cuda.synchronize(dev)
     ms = reduce_scalar(e0.elapsed_time(e1), "max", dev)
     ok = bool(torch.equal(h_out[0, :64, :64], src_t[0, :64, :64].t().contiguous()))
-    return {"value": round(2 * nbytes * world * steps / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
+    ceil = pcie_ceiling(torch, dev, h_in, h_out)
+    value = 2 * nbytes * world * steps / (ms / 1e3) / 1e9
+    return {"value": round(value, 3), "unit": "GB/s",
+            "pcie_ceiling": {"value": round(ceil * world, 3), "unit": "GB/s",
+                             "frac": round(value / (ceil * world), 4),
+                             "what": "the same bytes as one plain H2D copy and one plain D2H "
+                                     "copy running concurrently on two streams (no "
+                                     "transpose): the bound the e2e path can reach"},
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps,
             "gpu_launches": launches[0], "spot_check": "ok" if ok else "MISMATCH",
             "path": "desc_transpose_host (C-ABI): pinned host -> banded H2D | transpose | D2H "
