@@ -454,7 +454,9 @@ scan_aggregates_kernel(const Acc *__restrict__ agg, Acc *__restrict__ excl, int6
         __syncthreads();
         if (warp == 0) wt[lane] = warp_incl_scan(wt[lane], lane);   // inclusive over warps
         __syncthreads();
-        Acc run = carry_s + (warp ? wt[warp - 1] : Acc(0)) + wi - tsum;
+        // exclusive prefix by a shuffle of the inclusive one, never wi - tsum (an inf or NaN
+        // aggregate would poison the tiles before it: inf - inf, NaN - NaN)
+        Acc run = carry_s + (warp ? wt[warp - 1] : Acc(0)) + warp_excl_from_incl(wi, lane);
 #pragma unroll
         for (int k = 0; k < IT; ++k) {
             if (i0 + k < ntiles) excl[i0 + k] = run;
@@ -572,7 +574,10 @@ struct ScanStreamCfg {
     static constexpr int Q = QT + S + 2;               // tile metadata slots
     static constexpr int WCOLS = 4 * VPT;              // TMEM columns per warp per tile
     static constexpr int TCOLS = (NR / 4) * WCOLS;     // TMEM columns per tile
-    static constexpr int HALF = (VPT + 1) / 2;         // scan warps: vectors per register pass
+#ifndef DESC_SCAN_PASS
+#define DESC_SCAN_PASS 2          // scan warps: register passes per tile (A/B knob)
+#endif
+    static constexpr int HALF = (VPT + DESC_SCAN_PASS - 1) / DESC_SCAN_PASS;   // vectors per pass
     static_assert(QT >= 2 && S >= 2, "need TMEM slack and a double-buffered ring");
     static_assert(NR % 4 == 0, "warp groups cover the four TMEM lane quarters evenly");
     static_assert(QT * TCOLS <= 512, "parked tiles must fit the 512 TMEM columns");
@@ -594,6 +599,10 @@ __device__ __forceinline__ uint64_t gtimer() {
 #define SCAN_TRACE(f, t, v) do { if ((uint64_t)(t) < (uint64_t)kTraceTiles) g_scan_trace[f][t] = (v); } while (0)
 #else
 #define SCAN_TRACE(f, t, v) do { } while (0)
+#endif
+
+#ifndef DESC_SCAN_CACHE       // 1: scan warps widen each element once and keep it (A/B knob)
+#define DESC_SCAN_CACHE 0
 #endif
 
 #ifndef DESC_SCAN_DIAG        // diagnostics builds only (wrong results): 1 = no look-back,
@@ -842,8 +851,22 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                 }
                 // the rounds' warp scans are independent: run them level by level together
                 Acc wi[H], wex[H], wt[H];
+#if DESC_SCAN_CACHE
+                // widen each element once (the conversions are the scan warps' busiest pipe)
+                Acc d[H][V];
+#pragma unroll
+                for (int v = 0; v < H; ++v) {
+                    wi[v] = 0;
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        d[v][e] = h + v < VPT ? to_acc<Acc>(unpack<In>(x[v], e)) : Acc(0);
+                        wi[v] += d[v][e];
+                    }
+                }
+#else
 #pragma unroll
                 for (int v = 0; v < H; ++v) wi[v] = h + v < VPT ? vec_sum<In, Acc>(x[v]) : Acc(0);
+#endif
                 warp_incl_scan_n<Acc, H>(wi, lane);
 #pragma unroll
                 for (int v = 0; v < H; ++v) {
@@ -860,7 +883,11 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                     uint4 o = make_uint4(0, 0, 0, 0);
 #pragma unroll
                     for (int e = 0; e < V; ++e) {
+#if DESC_SCAN_CACHE
+                        run += d[v][e];
+#else
                         run += to_acc<Acc>(unpack<In>(x[v], e));
+#endif
                         set_elem<In>(o, e, (In)run);
                     }
 #if DESC_SCAN_DIAG & 2

@@ -101,6 +101,42 @@ def test_scan_stream_many_tiles_per_cta(dt):
         _check_scan(y.cpu().numpy(), a, dt, algo)
 
 
+@pytest.mark.parametrize("algo", ["lookback", "three_pass", "stream"])
+def test_scan_f32_special_values(algo):
+    """f32 widening to the fp64 accumulator: the streaming scan converts normal numbers and
+    +-0 on the integer pipe and everything else with the conversion instruction, per 16-byte
+    vector -- mixed vectors of +-0, subnormals, the extreme normal exponents and ordinary
+    values must still meet the bound; an inf makes every later prefix inf, a NaN every later
+    prefix NaN, exactly as in the oracle."""
+    n = (1 << 22) + 5
+    rng = np.random.default_rng(7)
+    a = synth.random_floats(n, np.float32, 8)
+    kind = rng.integers(0, 8, n)
+    a[kind == 0] = 0.0
+    a[kind == 1] = -0.0
+    sub = rng.integers(1, 1 << 23, n).astype(np.uint32).view(np.float32)   # subnormals
+    a[kind == 2] = sub[kind == 2]
+    tiny = np.float32(np.finfo(np.float32).tiny)
+    a[kind == 3] = tiny * np.sign(rng.standard_normal(n)[kind == 3]).astype(np.float32)
+    a[kind == 4] = np.float32(1e30) * np.sign(rng.standard_normal(n)[kind == 4]).astype(np.float32)
+    x = torch.from_numpy(a).cuda()
+    y = desc.scan(x, algo=algo)
+    torch.cuda.synchronize()
+    _check_scan(y.cpu().numpy(), a, np.float32, algo)
+    for special in (np.inf, np.nan):
+        b = a.copy()
+        k = n // 3 + 1
+        b[k] = special
+        y = desc.scan(torch.from_numpy(b).cuda(), algo=algo).cpu().numpy()
+        ref = oracle.scan(b)
+        assert np.all(np.isfinite(y[:k])) and np.isnan(ref[k:]).any() == np.isnan(special)
+        if np.isnan(special):
+            assert np.all(np.isnan(y[k:]))
+        else:   # +inf plus finite terms below the f32 overflow stays +inf
+            assert np.array_equal(np.isinf(y[k:]), np.isinf(ref[k:].astype(np.float32)))
+        _check_scan(y[:k], b[:k], np.float32, (algo, special))
+
+
 def test_scan_in_place_and_repeat():
     a = synth.random_ints(1 << 20, np.int32, 4)
     x = torch.from_numpy(a).cuda()
