@@ -473,6 +473,24 @@ def ours_arm(args, wl, world, rank, local):
             parity = ("bit-exact vs oracle" if got.tobytes() == r["out"].tobytes()
                       else "MISMATCH vs oracle")
 
+    # ---- N > 1: the real exchange step as well (configs[4] at 32768^2, NCCL all-to-all) ---
+    exchange = None
+    # (ranks sharing one GPU over gloo -- the 1-GPU test of this code path -- can only take
+    # the IPC peer path: gloo has no CUDA all-to-all)
+    ximpl = "nccl" if bench_backend() == "nccl" else "p2p"
+    if world > 1 and args.exchange_n > 0 and (ximpl == "nccl" or os.environ.get("DESC_BENCH_EXCHANGE_P2P")):
+        try:
+            r = slab_exchange(world, rank, dev, args.exchange_n, ximpl, 20, 3)
+            exchange = {"workload": f"{args.exchange_n}x{args.exchange_n} f32 distributed "
+                                    f"transpose, row slabs + {ximpl} exchange (configs[4] "
+                                    "shape, smaller matrix)",
+                        "value": round(r["value"], 2), "unit": "GB/s",
+                        "ms_per_step": round(r["ms_max"] / 20, 4), "scaling": "strong",
+                        "roofline": r["roofline"], "parity": r["parity"],
+                        "gpu_launches": r["launches"]}
+        except Exception as e:  # the replica line above stands on its own
+            exchange = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     # ---- end to end through the public API with host buffers --------------------------
     e2e = None
     if not args.no_e2e:
@@ -511,6 +529,7 @@ def ours_arm(args, wl, world, rank, local):
             "parity": parity,
             "gpu_launches": launches,
             **({"small_problem": small} if small else {}),
+            **({"exchange": exchange} if exchange else {}),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -519,23 +538,17 @@ def ours_arm(args, wl, world, rank, local):
     return 0
 
 
-def dist_arm(args, wl, world, rank, local):
-    """configs[4]: the global M x N matrix lives as row slabs, one per rank; a step is one
-    full distributed transpose (slab_transpose over NCCL, or the fused IPC peer path)."""
+def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4):
+    """One distributed transpose of an n x n f32 matrix held as row slabs (configs[4]; NCCL
+    all-to-all path, or the fused IPC peer path): returns the measured figures.  The input is
+    the counter hash generated in HBM; parity is checked on sampled 64 x 64 blocks of every
+    rank's output slab against the oracle."""
     import torch
     import torch.distributed as dist
     import oracle
-    import paper_2305_03448_b200 as desc
     from paper_2305_03448_b200 import dist as ddist
 
-    local = local_device(local)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    desc.load()
-    if world > 1:
-        init_pg(dev)
-    M = N = args.dist_n
-    es = wl["es"]
+    M = N = n
     lay = ddist.SlabLayout(M, N, world, rank)
     seed = synth.BASE_SEED + 5
     x = torch.empty((lay.Rm, N), dtype=torch.int32, device=dev)
@@ -543,7 +556,7 @@ def dist_arm(args, wl, world, rank, local):
     x = x.view(torch.float32)
     out = torch.empty((lay.Rn, M), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    impl = args.dist_impl if world > 1 else "local"
+    impl = impl if world > 1 else "local"
     if impl == "p2p":
         xp = ddist.PeerSlabTranspose(out, M)
         step = lambda: xp(x)[1]                                      # noqa: E731
@@ -556,7 +569,7 @@ def dist_arm(args, wl, world, rank, local):
         def step():
             ddist.slab_transpose(x, out, workspace=ws)
             return 2 if world > 1 else 1                             # our kernels per step
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -564,23 +577,21 @@ def dist_arm(args, wl, world, rank, local):
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     ms_max = reduce_scalar(ms, "max", dev)
-    step_s = ms_max / args.steps / 1e3
-    total = 2 * M * N * es
-    value = total * args.steps / (ms_max / 1e3) / 1e9
+    step_s = ms_max / steps / 1e3
+    value = 2 * M * N * es * steps / (ms_max / 1e3) / 1e9
     peak, peak_src = load_peak()
     S = lay.Rm * N * es
     t_hbm = 2 * S / (peak * 1e9)
     t_nvl = lay.nvlink_bytes(es) / (NVLINK_PEER_GBS * 1e9)
     t_star = max(t_hbm, t_nvl)
-    # sampled parity: 64 x 64 blocks of this rank's output slab vs the oracle
     rng = np.random.default_rng(seed + rank)
     r0, _ = lay.out_rows()
     picks = [(0, 0), (lay.Rn - 64, M - 64)] + [
@@ -592,33 +603,58 @@ def dist_arm(args, wl, world, rank, local):
         got = out[j0:j0 + 64, i0:i0 + 64].view(torch.int32).cpu().numpy().view(np.uint32)
         ok &= got.tobytes() == exp.tobytes()
     all_ok = reduce_scalar(1.0 if ok else 0.0, "min", dev) > 0.5
+    if impl == "p2p":
+        xp.close()
+    del x, out
+    return {
+        "value": value, "ms_max": ms_max, "impl": impl, "launches": launches, "lay": lay,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm" if t_hbm >= t_nvl else "nvlink",
+                     "achieved": round((2 * S if t_hbm >= t_nvl else lay.nvlink_bytes(es))
+                                       / step_s / 1e9, 2),
+                     "peak": peak if t_hbm >= t_nvl else NVLINK_PEER_GBS,
+                     "unit": "GB/s", "frac": round(t_star / step_s, 4), "traffic": None,
+                     "t_star_ms": round(t_star * 1e3, 4), "t_hbm_ms": round(t_hbm * 1e3, 4),
+                     "t_nvlink_ms": round(t_nvl * 1e3, 4), "peak_source": peak_src,
+                     "note": "frac = T*/t_step, T* = max(2S/HBM, S(P-1)/P / 770 GB/s)"},
+        "parity": "sampled 64x64 blocks bit-exact vs oracle" if all_ok else "MISMATCH",
+    }
+
+
+def dist_arm(args, wl, world, rank, local):
+    """configs[4]: the global M x N matrix lives as row slabs, one per rank; a step is one
+    full distributed transpose (slab_transpose over NCCL, or the fused IPC peer path)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2305_03448_b200 as desc
+
+    local = local_device(local)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    desc.load()
+    if world > 1:
+        init_pg(dev)
+    r = slab_exchange(world, rank, dev, args.dist_n, args.dist_impl, args.steps, args.warmup,
+                      wl["es"])
+    lay = r["lay"]
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "metric": METRIC, "value": round(r["value"], 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "ms_per_step": round(r["ms_max"] / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"],
             "data": "synthetic (counter-based hash, generated in HBM)",
-            "config": {"workload": wl["name"], "rows": M, "cols": N, "ranks": world,
-                       "slab_rows": lay.Rm, "impl": impl,
+            "config": {"workload": wl["name"], "rows": lay.M, "cols": lay.N, "ranks": world,
+                       "slab_rows": lay.Rm, "impl": r["impl"],
                        "parallelism": f"row slabs over {world} rank(s)",
                        "l2": "inputs larger than L2, no flush",
                        "timing": "CUDA events around K steps, max over ranks"},
-            "roofline": {"bound": "hbm" if t_hbm >= t_nvl else "nvlink",
-                         "achieved": round((2 * S if t_hbm >= t_nvl else lay.nvlink_bytes(es))
-                                           / step_s / 1e9, 2),
-                         "peak": peak if t_hbm >= t_nvl else NVLINK_PEER_GBS,
-                         "unit": "GB/s", "frac": round(t_star / step_s, 4), "traffic": None,
-                         "t_star_ms": round(t_star * 1e3, 4), "t_hbm_ms": round(t_hbm * 1e3, 4),
-                         "t_nvlink_ms": round(t_nvl * 1e3, 4), "peak_source": peak_src,
-                         "note": "frac = T*/t_step, T* = max(2S/HBM, S(P-1)/P / 770 GB/s)"},
-            "parity": "sampled 64x64 blocks bit-exact vs oracle" if all_ok else "MISMATCH",
-            "gpu_launches": launches, "cpu_baseline": None, "e2e": None,
-            "clocks": clk.summary(),
+            "roofline": r["roofline"],
+            "parity": r["parity"],
+            "gpu_launches": r["launches"], "cpu_baseline": None, "e2e": None,
+            "clocks": r["clocks"],
         }
         print(json.dumps(line), flush=True)
-    if impl == "p2p":
-        xp.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -889,6 +925,9 @@ def main():
     ap.add_argument("--dist-impl", choices=["nccl", "p2p"], default="nccl")
     ap.add_argument("--dist-n", type=int, default=65536)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange-n", type=int, default=32768,
+                    help="N > 1 default workload: also time one n x n slab transpose with the "
+                         "NCCL all-to-all (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

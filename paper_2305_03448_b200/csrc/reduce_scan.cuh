@@ -601,10 +601,6 @@ __device__ __forceinline__ uint64_t gtimer() {
 #define SCAN_TRACE(f, t, v) do { } while (0)
 #endif
 
-#ifndef DESC_SCAN_CACHE       // 1: scan warps widen each element once and keep it (A/B knob)
-#define DESC_SCAN_CACHE 0
-#endif
-
 #ifndef DESC_SCAN_DIAG        // diagnostics builds only (wrong results): 1 = no look-back,
 #define DESC_SCAN_DIAG 0      // 2 = outputs are the inputs (no scan arithmetic)
 #endif
@@ -851,22 +847,8 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                 }
                 // the rounds' warp scans are independent: run them level by level together
                 Acc wi[H], wex[H], wt[H];
-#if DESC_SCAN_CACHE
-                // widen each element once (the conversions are the scan warps' busiest pipe)
-                Acc d[H][V];
-#pragma unroll
-                for (int v = 0; v < H; ++v) {
-                    wi[v] = 0;
-#pragma unroll
-                    for (int e = 0; e < V; ++e) {
-                        d[v][e] = h + v < VPT ? to_acc<Acc>(unpack<In>(x[v], e)) : Acc(0);
-                        wi[v] += d[v][e];
-                    }
-                }
-#else
 #pragma unroll
                 for (int v = 0; v < H; ++v) wi[v] = h + v < VPT ? vec_sum<In, Acc>(x[v]) : Acc(0);
-#endif
                 warp_incl_scan_n<Acc, H>(wi, lane);
 #pragma unroll
                 for (int v = 0; v < H; ++v) {
@@ -883,11 +865,7 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                     uint4 o = make_uint4(0, 0, 0, 0);
 #pragma unroll
                     for (int e = 0; e < V; ++e) {
-#if DESC_SCAN_CACHE
-                        run += d[v][e];
-#else
                         run += to_acc<Acc>(unpack<In>(x[v], e));
-#endif
                         set_elem<In>(o, e, (In)run);
                     }
 #if DESC_SCAN_DIAG & 2
