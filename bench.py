@@ -473,29 +473,24 @@ def ours_arm(args, wl, world, rank, local):
             parity = ("bit-exact vs oracle" if got.tobytes() == r["out"].tobytes()
                       else "MISMATCH vs oracle")
 
-    # ---- N > 1: the real exchange step as well (configs[4] at 32768^2, NCCL all-to-all) ---
-    exchange = None
-    # (ranks sharing one GPU over gloo -- the 1-GPU test of this code path -- can only take
-    # the IPC peer path: gloo has no CUDA all-to-all)
-    ximpl = "nccl" if bench_backend() == "nccl" else "p2p"
-    if world > 1 and args.exchange_n > 0 and (ximpl == "nccl" or os.environ.get("DESC_BENCH_EXCHANGE_P2P")):
-        try:
-            r = slab_exchange(world, rank, dev, args.exchange_n, ximpl, 20, 3)
-            exchange = {"workload": f"{args.exchange_n}x{args.exchange_n} f32 distributed "
-                                    f"transpose, row slabs + {ximpl} exchange (configs[4] "
-                                    "shape, smaller matrix)",
-                        "value": round(r["value"], 2), "unit": "GB/s",
-                        "ms_per_step": round(r["ms_max"] / 20, 4), "scaling": "strong",
-                        "roofline": r["roofline"], "parity": r["parity"],
-                        "gpu_launches": r["launches"]}
-        except Exception as e:  # the replica line above stands on its own
-            exchange = {"error": f"{type(e).__name__}: {e}"[:300]}
-
     # ---- end to end through the public API with host buffers --------------------------
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, wl,
                           kernel, world)
+
+    # ---- N > 1: the real exchange step as well (configs[4] at 32768^2) --------------------
+    # NCCL all-to-all path (pipelined over row chunks; the unchunked variant timed beside it
+    # for A/B), then the fused peer-to-peer path (CUDA IPC, transposed blocks stored straight
+    # into the peers' slabs).  Ranks sharing one GPU over gloo (the 1-GPU test of this code
+    # path) can only take the peer path: gloo has no CUDA all-to-all.
+    exchange = exchange_p2p = None
+    nccl = bench_backend() == "nccl"
+    if world > 1 and args.exchange_n > 0:
+        if nccl:
+            exchange = exchange_object(world, rank, dev, args.exchange_n, "nccl")
+        if os.environ.get("DESC_BENCH_EXCHANGE_P2P", "1" if nccl else "0") == "1":
+            exchange_p2p = exchange_object(world, rank, dev, args.exchange_n, "p2p")
 
     if rank == 0:
         line = {
@@ -530,6 +525,7 @@ def ours_arm(args, wl, world, rank, local):
             "gpu_launches": launches,
             **({"small_problem": small} if small else {}),
             **({"exchange": exchange} if exchange else {}),
+            **({"exchange_p2p": exchange_p2p} if exchange_p2p else {}),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -538,7 +534,29 @@ def ours_arm(args, wl, world, rank, local):
     return 0
 
 
-def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4):
+def exchange_object(world, rank, dev, n, impl, steps=20, warmup=3):
+    """The `exchange` / `exchange_p2p` object of the N > 1 replica line: one n x n f32 slab
+    transpose over all ranks (strong scaling).  A Python-level failure is reported in the
+    object and leaves the replica line intact."""
+    try:
+        r = slab_exchange(world, rank, dev, n, impl, steps, warmup)
+        obj = {"workload": f"{n}x{n} f32 distributed transpose, row slabs + {impl} exchange "
+                           "(configs[4] shape, smaller matrix)",
+               "value": round(r["value"], 2), "unit": "GB/s",
+               "ms_per_step": round(r["ms_max"] / steps, 4), "scaling": "strong",
+               "roofline": r["roofline"], "parity": r["parity"], "gpu_launches": r["launches"]}
+        if impl == "nccl":
+            obj["chunks"] = r["chunks"]
+            if r["chunks"] > 1:   # A/B: the same exchange without the pipeline
+                r1 = slab_exchange(world, rank, dev, n, impl, steps, warmup, chunks=1)
+                obj["unchunked"] = {"ms_per_step": round(r1["ms_max"] / steps, 4),
+                                    "frac": r1["roofline"]["frac"], "parity": r1["parity"]}
+        return obj
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
+def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4, chunks=None):
     """One distributed transpose of an n x n f32 matrix held as row slabs (configs[4]; NCCL
     all-to-all path, or the fused IPC peer path): returns the measured figures.  The input is
     the counter hash generated in HBM; parity is checked on sampled 64 x 64 blocks of every
@@ -557,6 +575,7 @@ def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4):
     out = torch.empty((lay.Rn, M), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     impl = impl if world > 1 else "local"
+    C = None
     if impl == "p2p":
         xp = ddist.PeerSlabTranspose(out, M)
         step = lambda: xp(x)[1]                                      # noqa: E731
@@ -566,9 +585,11 @@ def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4):
             ws = (torch.empty(lay.Rm * N, dtype=torch.float32, device=dev),
                   torch.empty(lay.Rm * N, dtype=torch.float32, device=dev))
 
+        C = ddist.default_chunks(lay.Rm, world) if chunks is None else chunks
+
         def step():
-            ddist.slab_transpose(x, out, workspace=ws)
-            return 2 if world > 1 else 1                             # our kernels per step
+            ddist.slab_transpose(x, out, workspace=ws, chunks=C)
+            return 2 * C if world > 1 else 1                         # our kernels per step
     for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -608,6 +629,7 @@ def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4):
     del x, out
     return {
         "value": value, "ms_max": ms_max, "impl": impl, "launches": launches, "lay": lay,
+        "chunks": C,
         "clocks": clk.summary(),
         "roofline": {"bound": "hbm" if t_hbm >= t_nvl else "nvlink",
                      "achieved": round((2 * S if t_hbm >= t_nvl else lay.nvlink_bytes(es))
@@ -635,7 +657,7 @@ def dist_arm(args, wl, world, rank, local):
     if world > 1:
         init_pg(dev)
     r = slab_exchange(world, rank, dev, args.dist_n, args.dist_impl, args.steps, args.warmup,
-                      wl["es"])
+                      wl["es"], chunks=args.dist_chunks)
     lay = r["lay"]
     if rank == 0:
         line = {
@@ -645,7 +667,7 @@ def dist_arm(args, wl, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"],
             "data": "synthetic (counter-based hash, generated in HBM)",
             "config": {"workload": wl["name"], "rows": lay.M, "cols": lay.N, "ranks": world,
-                       "slab_rows": lay.Rm, "impl": r["impl"],
+                       "slab_rows": lay.Rm, "impl": r["impl"], "chunks": r["chunks"],
                        "parallelism": f"row slabs over {world} rank(s)",
                        "l2": "inputs larger than L2, no flush",
                        "timing": "CUDA events around K steps, max over ranks"},
@@ -923,6 +945,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--dist-impl", choices=["nccl", "p2p"], default="nccl")
+    ap.add_argument("--dist-chunks", type=int, default=None,
+                    help="pipeline depth of the NCCL slab transpose (default: dist.default_chunks)")
     ap.add_argument("--dist-n", type=int, default=65536)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange-n", type=int, default=32768,

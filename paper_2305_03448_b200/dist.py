@@ -16,7 +16,9 @@ Two implementations:
     2. ``all_to_all_single`` over NCCL (NVLink 5 / NVSwitch);
     3. unpack: the P received Rn x Rm blocks are placed side by side in out_r with
        ``desc_copy_batched`` (pitch M).
-  Per-rank HBM traffic ~6 S (S = slab bytes), NVLink S (P-1)/P each direction.
+  Per-rank HBM traffic ~6 S (S = slab bytes), NVLink S (P-1)/P each direction.  The three
+  steps are pipelined over C row chunks of the slab so that the all-to-all (NVLink-bound)
+  overlaps the local passes (HBM-bound).
 
 * ``PeerSlabTranspose`` -- fused peer-to-peer path: every rank maps the
   other ranks' output slabs with CUDA IPC once; a call launches the TMA transpose kernel
@@ -82,19 +84,42 @@ def _cuda_transpose(src, dst):
     desc.transpose(src, dst)
 
 
-def _cuda_unpack(recv, out, P, Rn, Rm, M):
-    """out[:, s*Rm:(s+1)*Rm] = recv[s] for s < P  (recv: P x Rn x Rm contiguous)."""
-    desc.desc_copy_batched(recv.data_ptr(), out.data_ptr(), P, Rn, Rm, Rm, M, Rn * Rm, Rm,
-                           recv.dtype, torch.cuda.current_stream(recv.device).cuda_stream)
+def _cuda_unpack(recv, out, P, Rn, c, M, col0=0, Rm=None):
+    """out[:, s*Rm + col0 : s*Rm + col0 + c] = recv[s] for s < P  (recv: P x Rn x c contiguous;
+    Rm defaults to c, i.e. the unchunked exchange)."""
+    Rm = c if Rm is None else Rm
+    es = out.element_size()
+    desc.desc_copy_batched(recv.data_ptr(), out.data_ptr() + col0 * es, P, Rn, c, c, M, Rn * c,
+                           Rm, recv.dtype, torch.cuda.current_stream(recv.device).cuda_stream)
+
+
+def default_chunks(Rm: int, P: int) -> int:
+    """Pipeline depth of the NCCL path: 4 chunks of >= 128 slab rows when they divide Rm."""
+    if P == 1:
+        return 1
+    for C in (4, 2):
+        if Rm % C == 0 and Rm // C >= 128:
+            return C
+    return 1
 
 
 def slab_transpose(in_slab: torch.Tensor, out_slab: torch.Tensor | None = None, group=None,
-                   local_transpose=None, local_copy=None, workspace=None):
+                   local_transpose=None, local_copy=None, workspace=None, chunks=None,
+                   all_to_all=None):
     """Transpose the global matrix whose row slab this rank holds (NCCL all-to-all path).
 
     in_slab: (Rm, N) contiguous, this rank's rows of the M x N input (M = Rm * P).
     returns out_slab: (Rn, M), this rank's rows of the N x M transpose (Rn = N / P).
-    workspace: optional (send, recv) pair of tensors with N * Rm elements each."""
+    workspace: optional (send, recv) pair of tensors with N * Rm elements each.
+    chunks: C, the pipeline depth (default ``default_chunks``).  The slab is cut into C row
+      chunks of c = Rm / C rows; chunk k is transposed into its own send buffer (N x c: its row
+      band s is block (r, s)'s chunk, transposed), exchanged with an asynchronous all-to-all,
+      and unpacked into out_r[:, s*Rm + k*c : ... + c].  All C transposes are issued first, so
+      the all-to-all of chunk k overlaps the transposes of the later chunks and the unpacks of
+      the earlier ones (the NCCL collective runs on its own stream); the result does not depend
+      on C.
+    all_to_all: the exchange primitive (default ``torch.distributed.all_to_all_single``); an
+      injection point for the single-GPU multi-process test only."""
     P = dist.get_world_size(group) if dist.is_initialized() else 1
     r = dist.get_rank(group) if dist.is_initialized() else 0
     Rm, N = in_slab.shape
@@ -104,22 +129,35 @@ def slab_transpose(in_slab: torch.Tensor, out_slab: torch.Tensor | None = None, 
         raise ValueError("in_slab must be contiguous")
     if out_slab is None:
         out_slab = torch.empty((Rn, M), dtype=in_slab.dtype, device=in_slab.device)
-    if tuple(out_slab.shape) != (Rn, M):
-        raise ValueError(f"out_slab must be {(Rn, M)}")
+    if tuple(out_slab.shape) != (Rn, M) or not out_slab.is_contiguous():
+        raise ValueError(f"out_slab must be contiguous {(Rn, M)}")
     local_transpose = local_transpose or _cuda_transpose
     local_copy = local_copy or _cuda_unpack
+    all_to_all = all_to_all or dist.all_to_all_single
     if P == 1:
         local_transpose(in_slab, out_slab)
         return out_slab
+    C = default_chunks(Rm, P) if chunks is None else int(chunks)
+    if C < 1 or Rm % C:
+        raise ValueError(f"chunks={C} must divide the slab rows Rm={Rm}")
+    c = Rm // C
     if workspace is None:
-        send = torch.empty((N, Rm), dtype=in_slab.dtype, device=in_slab.device)
-        recv = torch.empty((P, Rn, Rm), dtype=in_slab.dtype, device=in_slab.device)
+        send = torch.empty(N * Rm, dtype=in_slab.dtype, device=in_slab.device)
+        recv = torch.empty(N * Rm, dtype=in_slab.dtype, device=in_slab.device)
     else:
-        send, recv = workspace
-        send, recv = send.view(N, Rm), recv.view(P, Rn, Rm)
-    local_transpose(in_slab, send)                       # T_r = in_r^T; band s = block (r, s)^T
-    dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
-    local_copy(recv, out_slab, P, Rn, Rm, M)             # out_r[:, s*Rm:(s+1)*Rm] = recv[s]
+        send, recv = (w.view(-1) for w in workspace)
+        if send.numel() < N * Rm or recv.numel() < N * Rm:
+            raise ValueError("workspace tensors need N * Rm elements each")
+    works = []
+    for k in range(C):
+        send_k = send[k * N * c:(k + 1) * N * c]
+        recv_k = recv[k * N * c:(k + 1) * N * c]
+        local_transpose(in_slab[k * c:(k + 1) * c], send_k.view(N, c))   # band s = (r,s)_k^T
+        works.append(all_to_all(recv_k, send_k, group=group, async_op=True))
+    for k in range(C):
+        works[k].wait()                      # NCCL: the compute stream waits for chunk k only
+        recv_k = recv[k * N * c:(k + 1) * N * c].view(P, Rn, c)
+        local_copy(recv_k, out_slab, P, Rn, c, M, k * c, Rm)   # out_r[:, s*Rm + k*c ..] = recv_k[s]
     return out_slab
 
 
@@ -132,7 +170,8 @@ class PeerSlabTranspose:
     any rank reads its slab).  Works with any process-group backend for the handle exchange
     (gloo in the single-GPU two-process test, NCCL in bench.py)."""
 
-    def __init__(self, out_slab: torch.Tensor, M: int, group=None, kernel: str = "auto"):
+    def __init__(self, out_slab: torch.Tensor, M: int, group=None, kernel: str = "auto",
+                 remote_kernel: str = "tma"):
         if not out_slab.is_cuda or not out_slab.is_contiguous():
             raise ValueError("out_slab must be a contiguous CUDA tensor")
         self.group = group
@@ -145,10 +184,15 @@ class PeerSlabTranspose:
         self.lay = SlabLayout(M, Rn * self.P, self.P, self.r)
         handle, offset = desc.desc_ipc_handle(out_slab.data_ptr())
         handles = [None] * self.P
-        dist.all_gather_object(handles, (handle, offset), group=group)
+        dist.all_gather_object(handles, (handle, offset, out_slab.device.index), group=group)
+        # blocks for a slab on ANOTHER GPU go through the TMA-load + st.global kernel (16-byte
+        # stores over NVLink); the TMA-store kernel is kept for same-device slabs, where its
+        # tensor map addresses local HBM
+        self.kernels = [kernel if d == out_slab.device.index else remote_kernel
+                        for (_, _, d) in handles]
         self.peer_ptr = []
         self._opened = []
-        for s, (h, off) in enumerate(handles):
+        for s, (h, off, _) in enumerate(handles):
             if s == self.r:
                 self.peer_ptr.append(out_slab.data_ptr())
             else:
@@ -172,7 +216,7 @@ class PeerSlabTranspose:
             src = in_slab.data_ptr() + s * lay.Rn * es                       # block (r, s)
             dst = self.peer_ptr[s] + self.r * lay.Rm * es                    # out_s[:, r*Rm]
             desc.desc_transpose_ex(src, dst, 1, lay.Rm, lay.Rn, lay.N, lay.M, 0, 0,
-                                   in_slab.dtype, self.kernel, stream)
+                                   in_slab.dtype, self.kernels[s], stream)
             launches += desc.desc_last_launch_count()
         if barrier:
             torch.cuda.current_stream(in_slab.device).synchronize()

@@ -48,6 +48,32 @@ def test_fake_ranks_exchange(P, shape):
         assert out.tobytes() == oracle.dist_expected_slab(A, r, P).tobytes()
 
 
+@pytest.mark.parametrize("P,C", [(2, 1), (2, 2), (4, 4), (8, 2)])
+def test_fake_ranks_chunked_exchange(P, C):
+    """The pipelined variant (C row chunks per slab, an all-to-all per chunk) simulated with P
+    numpy ranks: chunk k of rank s lands at out_r[:, s*Rm + k*c : s*Rm + (k+1)*c]."""
+    M, N = 64 * P, 48 * P
+    A = synth.random_bits((M, N), 4, 77 + P * C)
+    Rm, Rn = M // P, N // P
+    c = Rm // C
+    outs = [np.empty((Rn, M), dtype=A.dtype) for _ in range(P)]
+    for k in range(C):
+        sends = [oracle.transpose(A[r * Rm + k * c:r * Rm + (k + 1) * c]) for r in range(P)]
+        for r in range(P):
+            for s in range(P):
+                outs[r][:, s * Rm + k * c:s * Rm + (k + 1) * c] = sends[s][r * Rn:(r + 1) * Rn]
+    for r in range(P):
+        assert outs[r].tobytes() == oracle.dist_expected_slab(A, r, P).tobytes()
+
+
+def test_default_chunks_and_bad_chunks():
+    assert ddist.default_chunks(8192, 8) == 4 and ddist.default_chunks(8192, 1) == 1
+    assert ddist.default_chunks(256, 2) == 2 and ddist.default_chunks(100, 2) == 1
+    x = torch.zeros((6, 8), dtype=torch.int32)
+    with pytest.raises(ValueError):    # P = 1 never chunks, but the out shape is still checked
+        ddist.slab_transpose(x, torch.zeros((6, 6), dtype=torch.int32))
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -58,12 +84,13 @@ def _cpu_transpose(src, dst):           # oracle-backed local step (test only)
     dst.copy_(torch.from_numpy(oracle.transpose(src.numpy())))
 
 
-def _cpu_unpack(recv, out, P, Rn, Rm, M):
+def _cpu_unpack(recv, out, P, Rn, c, M, col0=0, Rm=None):
+    Rm = c if Rm is None else Rm
     for s in range(P):
-        out[:, s * Rm:(s + 1) * Rm] = recv[s]
+        out[:, s * Rm + col0:s * Rm + col0 + c] = recv[s]
 
 
-def _worker(rank, world, port, M, N, q):
+def _worker(rank, world, port, M, N, q, chunks=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -71,14 +98,18 @@ def _worker(rank, world, port, M, N, q):
         A = synth.random_bits((M, N), 4, 1234)         # every rank can build the global input
         Rm = M // world
         slab = torch.from_numpy(A[rank * Rm:(rank + 1) * Rm].view(np.int32).copy())
-        out = ddist.slab_transpose(slab, local_transpose=_cpu_transpose, local_copy=_cpu_unpack)
-        ok = out.numpy().view(np.uint32).tobytes() == oracle.dist_expected_slab(A, rank, world).tobytes()
+        exp = oracle.dist_expected_slab(A, rank, world).tobytes()
+        ok = True
+        for C in ([chunks] if chunks is not None else [None, 1, 2, 4]):
+            out = ddist.slab_transpose(slab, local_transpose=_cpu_transpose,
+                                       local_copy=_cpu_unpack, chunks=C)
+            ok &= out.numpy().view(np.uint32).tobytes() == exp
         q.put((rank, ok))
     finally:
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,M,N", [(2, 64, 96), (4, 128, 64)])
+@pytest.mark.parametrize("world,M,N", [(2, 64, 96), (4, 128, 64), (2, 1024, 256)])
 def test_gloo_slab_transpose(world, M, N):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

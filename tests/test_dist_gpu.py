@@ -100,3 +100,63 @@ def test_peer_slab_transpose_two_processes_one_gpu(world, M, N, es):
     for p in procs:
         p.join(timeout=60)
     assert res == {r: True for r in range(world)}
+
+
+class _Done:
+    def wait(self):
+        return True
+
+
+def _staged_all_to_all(out, inp, group=None, async_op=False):
+    """The exchange of slab_transpose through host memory (gloo has no CUDA all-to-all and
+    NCCL refuses two ranks on one GPU): test plumbing only, the local steps stay on the GPU."""
+    torch.cuda.synchronize()
+    o = torch.empty(out.shape, dtype=out.dtype)
+    tdist.all_to_all_single(o, inp.cpu(), group=group)
+    out.copy_(o)
+    return _Done()
+
+
+def _nccl_path_worker(rank, world, port, M, N, es, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.random_bits((M, N), es, 91)
+        it = {4: np.int32, 8: np.int64}[es]
+        Rm, Rn = M // world, N // world
+        slab = torch.from_numpy(A[rank * Rm:(rank + 1) * Rm].view(it).copy()).cuda()
+        exp = oracle.dist_expected_slab(A, rank, world).tobytes()
+        ws = (torch.empty(Rm * N, dtype=slab.dtype, device="cuda"),
+              torch.empty(Rm * N, dtype=slab.dtype, device="cuda"))
+        ok = True
+        for C in (None, 1, 2, 4):
+            out = torch.full((Rn, M), -1, dtype=slab.dtype, device="cuda")
+            ddist.slab_transpose(slab, out, workspace=ws, chunks=C,
+                                 all_to_all=_staged_all_to_all)
+            torch.cuda.synchronize()
+            ok &= out.cpu().numpy().view(A.dtype).tobytes() == exp
+        q.put((rank, bool(ok)))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,M,N,es", [(2, 1024, 768, 4), (4, 1024, 512, 8)])
+def test_slab_transpose_chunked_processes_one_gpu(world, M, N, es):
+    """The NCCL path's local steps (chunked transpose into the send buffer, side-by-side unpack
+    at column offset k*c) on the GPU in `world` processes; the all-to-all itself is staged
+    through the host."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_path_worker, args=(r, world, port, M, N, es, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}
