@@ -37,7 +37,8 @@ METRIC = "transpose effective GB/s (read+write) and % of HBM peak at 1/2/4/8 B20
 L2_BYTES = 126 * 1024 * 1024
 KERNEL_FN = {"tma_st": "desc::transpose_tma2_kernel (TMA load + TMA store)",
              "tma": "desc::transpose_tma_kernel (TMA load + st.global)",
-             "smem": "desc::transpose_smem_kernel (32x33 smem tile)"}
+             "smem": "desc::transpose_smem_kernel (32x33 smem tile)",
+             "tiled": "desc::transpose_tiled_kernel (64x65 smem tile, 16 loads in flight)"}
 
 WORKLOADS = {
     "8192f32": dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4,
@@ -50,6 +51,11 @@ WORKLOADS = {
                     name="4096x4096 f64 transpose (paper-size extra: 256 MB in+out, P:1051)"),
     "8192f64": dict(batch=1, rows=8192, cols=8192, dtype="f64", es=8,
                     name="8192x8192 f64 transpose (paper-size extra: 1 GiB in+out, P:1051)"),
+    "3000x5000f64_ld5001": dict(batch=1, rows=3000, cols=5000, dtype="f64", es=8, ld_in=5001,
+                                name="3000x5000 f64 with ld_in = 5001 (TMA-ineligible: 40008-byte pitch; "
+                                     "BASELINE.json configs[2] fallback variant)"),
+    "8192f32_ld8193": dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4, ld_in=8193,
+                           name="8192x8192 f32 with ld_in = 8193 (TMA-ineligible pitch)"),
     "batched": dict(batch=256, rows=1024, cols=1024, dtype="f32", es=4, shard=True,
                     name="batched 256x(1024x1024) f32, batch sharded over ranks (BASELINE.json configs[3])"),
     "dist65536": dict(batch=1, rows=65536, cols=65536, dtype="f32", es=4, dist=True,
@@ -369,7 +375,13 @@ def ours_arm(args, wl, world, rank, local):
     # seeded synthetic input, generated on the host (so the oracle sees the same bits)
     src = synth.random_bits((batch, rows, cols), es, synth.BASE_SEED + 2 + 1000 * rank)
     src_t = torch.from_numpy(src.view(np.int32 if es == 4 else np.int64))
-    x = src_t.to(dev).view(tdt)
+    ld_in = wl.get("ld_in", cols)
+    if ld_in == cols:
+        x = src_t.to(dev).view(tdt)
+    else:          # padded input pitch (TMA-ineligible workloads): logical rows x cols view
+        xp = torch.zeros((batch, rows, ld_in), dtype=src_t.dtype, device=dev)
+        xp[:, :, :cols] = src_t.to(dev)
+        x = xp.view(tdt)
     y = torch.empty((batch, cols, rows), dtype=tdt, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
@@ -387,15 +399,15 @@ def ours_arm(args, wl, world, rank, local):
 
     def step():
         if batch == 1:
-            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), 1, rows, cols, cols, rows, 0, 0,
+            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), 1, rows, cols, ld_in, rows, 0, 0,
                                    wl["dtype"], kernel, sptr)
         else:
-            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), batch, rows, cols, cols, rows,
-                                   rows * cols, rows * cols, wl["dtype"], kernel, sptr)
+            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), batch, rows, cols, ld_in, rows,
+                                   rows * ld_in, rows * cols, wl["dtype"], kernel, sptr)
         return desc.desc_last_launch_count()
 
-    selected = desc.desc_select_kernel(x.data_ptr(), y.data_ptr(), batch, rows, cols, cols, rows,
-                                       rows * cols if batch > 1 else 0,
+    selected = desc.desc_select_kernel(x.data_ptr(), y.data_ptr(), batch, rows, cols, ld_in, rows,
+                                       rows * ld_in if batch > 1 else 0,
                                        rows * cols if batch > 1 else 0, wl["dtype"])
     if kernel != "auto":
         selected = kernel
@@ -499,7 +511,7 @@ def ours_arm(args, wl, world, rank, local):
             "ms_per_step": round(timed_ms_max / args.steps, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": wl["dtype"], "data": "synthetic (seeded random bit patterns, host-generated)",
-            "config": {"workload": wl["name"], "rows": rows, "cols": cols,
+            "config": {"workload": wl["name"], "rows": rows, "cols": cols, "ld_in": ld_in,
                        "batch_per_gpu": batch, "kernel": selected,
                        "parallelism": f"{world} independent replica(s), no collective",
                        "l2": ("flushed before every step (read of a 252 MiB buffer, untimed)" if flush else
@@ -937,7 +949,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="8192f32")
-    ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem", "tiled"], default="auto")
     ap.add_argument("--scan-algo", choices=["auto", "lookback", "three_pass", "stream"],
                     default="auto")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)

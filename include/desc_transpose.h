@@ -78,12 +78,17 @@ typedef enum desc_dtype {
     DESC_F16 = 4, DESC_BF16 = 5, DESC_U8 = 6
 } desc_dtype;
 
-/* Kernel variants (desc_transpose_ex).  AUTO picks TMA_ST when the alignment rules
- * below hold and the element size is 4 or 8 with rows*size >= 16, else TMA when the
- * alignment rules hold, else SMEM.
+/* Kernel variants (desc_transpose_ex).  AUTO picks TILED for 4/8-byte cells when rows
+ * and cols are both >= 64 (measured fastest there) and whenever the TMA alignment rules
+ * below fail; otherwise TMA_ST when the element size is 4 or 8 with rows*size >= 16,
+ * else TMA.
  *   DESC_KERNEL_SMEM : 32x32 shared-memory tile, padded [32][33], 32x8 threads,
  *                      predicated edges -- the corrected Listing 1 schedule
- *                      (P:49-60 with the P:44 fix).  Any alignment.
+ *                      (P:49-60 with the P:44 fix).  Any alignment.  Kept as the
+ *                      paper's schedule (baseline); AUTO never picks it.
+ *   DESC_KERNEL_TILED : any alignment; 64x64 (8-byte cells: 64x32) tiles padded by one
+ *                      cell, 256 threads each issuing all of its 16 (8) cell loads
+ *                      before staging, one tile per CTA, predicated edge tiles.
  *   DESC_KERNEL_TMA  : persistent, warp-specialised: TMA (cp.async.bulk.tensor)
  *                      loads of 128-byte-swizzled tiles into a multi-stage
  *                      mbarrier ring, conflict-free 16-byte shared reads,
@@ -99,7 +104,8 @@ typedef enum desc_kernel {
     DESC_KERNEL_AUTO = 0,
     DESC_KERNEL_SMEM = 1,
     DESC_KERNEL_TMA = 2,
-    DESC_KERNEL_TMA_ST = 3
+    DESC_KERNEL_TMA_ST = 3,
+    DESC_KERNEL_TILED = 4
 } desc_kernel;
 
 /* Single transpose: in (rows x cols, pitch ld_in) -> out (cols x rows, pitch ld_out). */
@@ -123,7 +129,7 @@ desc_status desc_transpose_ex(const void *in, void *out, int64_t batch,
                               desc_kernel kernel, void *stream);
 
 /* The variant AUTO would run for these arguments (no launch, no pointer
- * checks beyond alignment).  Returns DESC_KERNEL_SMEM, _TMA or _TMA_ST. */
+ * checks beyond alignment).  Returns DESC_KERNEL_TILED, _TMA or _TMA_ST. */
 desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
                                int64_t rows, int64_t cols, int64_t ld_in,
                                int64_t ld_out, int64_t stride_in,

@@ -16,6 +16,7 @@
 
 #include "../../include/desc_transpose.h"
 #include "smem_transpose.cuh"
+#include "tiled_transpose.cuh"
 #include "tma_transpose.cuh"
 #include "tma_store_transpose.cuh"
 #include "copy_kernel.cuh"
@@ -442,6 +443,36 @@ desc_status launch_smem(const Args &a) {
     return DESC_OK;
 }
 
+template <typename Cell>
+desc_status launch_tiled(const Args &a) {
+    using C = desc::TiledCfg<Cell>;
+    const int64_t tiles_r = (a.rows + C::TR - 1) / C::TR, tiles_c = (a.cols + C::TC - 1) / C::TC;
+    const int64_t ntiles = tiles_r * tiles_c * a.batch;
+    const int64_t max_grid = (int64_t)1 << 30;           // one tile per CTA up to 2^30 tiles
+    const int grid = (int)(ntiles < max_grid ? ntiles : max_grid);
+    if (C::SMEM > 48 * 1024) {
+        static std::mutex mu;                              // per device, once
+        static bool opted[64] = {};
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 64 || !opted[dev]) {
+            e = cudaFuncSetAttribute(desc::transpose_tiled_kernel<Cell>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tiled smem)");
+            if (dev < 64) opted[dev] = true;
+        }
+    }
+    desc::transpose_tiled_kernel<Cell><<<grid, 256, C::SMEM, a.stream>>>(
+        static_cast<const Cell *>(a.in), static_cast<Cell *>(a.out), a.rows, a.cols, a.ld_in,
+        a.ld_out, a.stride_in, a.stride_out, tiles_r, tiles_c, ntiles);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "transpose_tiled_kernel launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
 // Development knob: DESC_TMA_CFG=<n> selects a tile/pipeline configuration for A/B
 // measurement (read once).  The default (0) is the tuned configuration.
 int tma_cfg() {
@@ -532,6 +563,16 @@ desc_status run_tma2(const Args &a) {
     return fail(DESC_ERR_KERNEL, "TMA-store kernel supports 4- and 8-byte elements only");
 }
 
+desc_status run_tiled(const Args &a) {
+    switch (a.es) {
+        case 4: return launch_tiled<uint32_t>(a);
+        case 8: return launch_tiled<unsigned long long>(a);
+        case 2: return launch_tiled<uint16_t>(a);
+        case 1: return launch_tiled<uint8_t>(a);
+        default: return fail(DESC_ERR_DTYPE, "unsupported element size %d", a.es);
+    }
+}
+
 desc_status run_smem(const Args &a) {
     switch (a.es) {
         case 4: return launch_smem<uint32_t>(a);
@@ -603,6 +644,14 @@ desc_status validate(const Args &a, bool *empty) {
     return DESC_OK;
 }
 
+// AUTO's choice for 4/8-byte cells (scripts/exp_auto.py, profiles/r01_exp_auto.txt): the
+// TILED kernel reaches the copy ceiling on every 2-D shape whose sides both hold a whole
+// 64-cell tile; TMA keeps the skinny shapes (a side < 64 wastes most of a TILED tile) and
+// 1/2-byte cells (TILED's cell-wide accesses move only 32/64 bytes per warp instruction).
+bool tiled_preferred(const Args &a) {
+    return (a.es == 4 || a.es == 8) && a.rows >= 64 && a.cols >= 64;
+}
+
 desc_status dispatch(const Args &a, desc_kernel k) {
     const bool tma_ok = tma_eligible(a);
     if (a.rev_rows) {   // only the TMA-store kernel reads rows mirrored
@@ -617,7 +666,9 @@ desc_status dispatch(const Args &a, desc_kernel k) {
     if (k == DESC_KERNEL_TMA_ST && !tma_store_ok(a))
         return fail(DESC_ERR_KERNEL, "TMA-store kernel needs 4/8-byte elements and rows*size >= 16");
     if (k == DESC_KERNEL_TMA_ST) return run_tma2(a);
-    if (k == DESC_KERNEL_SMEM || (k == DESC_KERNEL_AUTO && !tma_ok)) return run_smem(a);
+    if (k == DESC_KERNEL_SMEM) return run_smem(a);
+    if (k == DESC_KERNEL_TILED || (k == DESC_KERNEL_AUTO && (!tma_ok || tiled_preferred(a))))
+        return run_tiled(a);
     if (k == DESC_KERNEL_AUTO && tma_store_ok(a)) return run_tma2(a);
     if (k == DESC_KERNEL_TMA || k == DESC_KERNEL_AUTO) return run_tma(a);
     return fail(DESC_ERR_KERNEL, "unknown kernel variant %d", (int)k);
@@ -1352,7 +1403,7 @@ desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch, i
                                int64_t stride_out, desc_dtype dtype) {
     Args a{in, const_cast<void *>(out), batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
            dtype_size(dtype), nullptr};
-    if (a.es == 0 || !tma_eligible(a)) return DESC_KERNEL_SMEM;
+    if (a.es == 0 || !tma_eligible(a) || tiled_preferred(a)) return DESC_KERNEL_TILED;
     return tma_store_ok(a) ? DESC_KERNEL_TMA_ST : DESC_KERNEL_TMA;
 }
 

@@ -1,0 +1,122 @@
+// tiled_transpose.cuh -- the alignment-agnostic transpose for B200 (DESC_KERNEL_TILED).
+//
+// Same operation as every other variant (caption P:108): out[j][i] = in[i][j].
+// Taken by AUTO whenever the TMA rules reject the arguments (a base that is not 16-byte
+// aligned, ld*size or stride*size not a multiple of 16 -- e.g. 3000 x 5000 f64 with
+// ld_in = 5001, BASELINE configs[2] variant), where no vector or bulk access is legal, so the
+// kernel has to reach HBM bandwidth with cell-wide accesses.  What differs from the paper's
+// Listing 1 schedule (transpose_smem_kernel, kept as the faithful baseline):
+//   * a TR x TC tile (64 x 64 cells for 1/2/4-byte cells, 64 x 32 for 8-byte cells), so a
+//     warp row is 128 / 256 contiguous bytes on both sides,
+//   * every thread issues all of its TR*TC/256 loads (16 for f32) back to back into
+//     registers before touching shared memory: 16 independent HBM requests in flight per
+//     thread instead of Listing 1's one-at-a-time load/store pairs (B200 needs ~40 KB in
+//     flight per SM to cover HBM latency at 6.5 TB/s),
+//   * the staging tile is padded to TC + 1 cells: the column read of the copy-out hits 32
+//     distinct banks (4-byte cells: lane*(TC+1) = lane mod 32; 8-byte cells: per half-warp
+//     2*lane mod 32, each access covering two banks),
+//   * one tile per CTA, 1-D grid (the block scheduler balances the SMs), interior tiles with
+//     no predicates, edge tiles predicated (R6).
+#pragma once
+#include <cstdint>
+
+namespace desc {
+
+// A/B knobs (scripts/build_tiled_variants.py): tile rows / cols for 8-byte and narrower cells
+#ifndef DESC_TILED_TR8
+#define DESC_TILED_TR8 64
+#endif
+#ifndef DESC_TILED_TC8
+#define DESC_TILED_TC8 64
+#endif
+#ifndef DESC_TILED_TR4
+#define DESC_TILED_TR4 64
+#endif
+#ifndef DESC_TILED_TC4
+#define DESC_TILED_TC4 64
+#endif
+
+template <typename Cell>
+struct TiledCfg {
+    static constexpr bool W8 = sizeof(Cell) == 8;
+    static constexpr int TR = W8 ? DESC_TILED_TR8 : DESC_TILED_TR4;   // tile rows (input)
+    static constexpr int TC = W8 ? DESC_TILED_TC8 : DESC_TILED_TC4;   // tile cols (input)
+    static constexpr int CW = TC / 32;                      // column groups per lane
+    static constexpr int RK = TR / 8;                       // rows per warp
+    static constexpr int SMEM = TR * (TC + 1) * (int)sizeof(Cell);   // padded staging tile
+};
+
+template <typename Cell>
+__global__ void __launch_bounds__(256)
+transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int64_t rows,
+                       int64_t cols, int64_t ld_in, int64_t ld_out, int64_t stride_in,
+                       int64_t stride_out, int64_t tiles_r, int64_t tiles_c, int64_t ntiles) {
+    using C = TiledCfg<Cell>;
+    constexpr int TR = C::TR, TC = C::TC, CW = C::CW, RK = C::RK;
+    extern __shared__ __align__(16) unsigned char tiled_smem[];
+    Cell(*tile)[TC + 1] = reinterpret_cast<Cell(*)[TC + 1]>(tiled_smem);
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t tiles_per_mat = tiles_r * tiles_c;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t bt = t / tiles_per_mat;
+        const int64_t rem = t - bt * tiles_per_mat;
+        const int64_t ti = rem / tiles_c, tj = rem - ti * tiles_c;
+        const int64_t r0 = ti * TR, c0 = tj * TC;
+        const Cell *src = in + bt * stride_in + r0 * ld_in + c0;
+        Cell *dst = out + bt * stride_out + c0 * ld_out + r0;
+        const bool full = r0 + TR <= rows && c0 + TC <= cols;
+        Cell v[RK][CW];
+        if (full) {
+#pragma unroll
+            for (int k = 0; k < RK; ++k)
+#pragma unroll
+                for (int g = 0; g < CW; ++g) v[k][g] = src[(int64_t)(ty + 8 * k) * ld_in + tx + 32 * g];
+#pragma unroll
+            for (int k = 0; k < RK; ++k)
+#pragma unroll
+                for (int g = 0; g < CW; ++g) tile[ty + 8 * k][tx + 32 * g] = v[k][g];
+        } else {
+            const int nr = (int)(rows - r0 < TR ? rows - r0 : TR);
+            const int nc = (int)(cols - c0 < TC ? cols - c0 : TC);
+#pragma unroll
+            for (int k = 0; k < RK; ++k)
+#pragma unroll
+                for (int g = 0; g < CW; ++g) {
+                    const int r = ty + 8 * k, c = tx + 32 * g;
+                    if (r < nr && c < nc) v[k][g] = src[(int64_t)r * ld_in + c];
+                }
+#pragma unroll
+            for (int k = 0; k < RK; ++k)
+#pragma unroll
+                for (int g = 0; g < CW; ++g) {
+                    const int r = ty + 8 * k, c = tx + 32 * g;
+                    if (r < nr && c < nc) tile[r][c] = v[k][g];
+                }
+        }
+        __syncthreads();
+        // copy-out: output row c0 + oc (= input column), 32 lanes x TR/32 cells contiguous
+        constexpr int OK = TC / 8, OH = TR / 32;
+        if (full) {
+#pragma unroll
+            for (int m = 0; m < OK; ++m)
+#pragma unroll
+                for (int h = 0; h < OH; ++h) {
+                    const int oc = ty + 8 * m, orr = tx + 32 * h;
+                    dst[(int64_t)oc * ld_out + orr] = tile[orr][oc];
+                }
+        } else {
+            const int nr = (int)(rows - r0 < TR ? rows - r0 : TR);
+            const int nc = (int)(cols - c0 < TC ? cols - c0 : TC);
+#pragma unroll
+            for (int m = 0; m < OK; ++m)
+#pragma unroll
+                for (int h = 0; h < OH; ++h) {
+                    const int oc = ty + 8 * m, orr = tx + 32 * h;
+                    if (oc < nc && orr < nr) dst[(int64_t)oc * ld_out + orr] = tile[orr][oc];
+                }
+        }
+        __syncthreads();                                  // tile reused by the next iteration
+    }
+}
+
+}  // namespace desc

@@ -1,0 +1,17 @@
+"""Compile-time variants of the TILED transpose kernel for A/B runs (DESC_LIB=<path>)."""
+import os, sys
+from concurrent.futures import ThreadPoolExecutor
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2305_03448_b200 import build as B
+
+VARIANTS = {
+    "a": ["DESC_TILED_TR8=128", "DESC_TILED_TC8=32", "DESC_TILED_TR4=64", "DESC_TILED_TC4=128"],
+    "b": ["DESC_TILED_TR8=128", "DESC_TILED_TC8=64", "DESC_TILED_TR4=32", "DESC_TILED_TC4=128"],
+    "c": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=128", "DESC_TILED_TR4=128", "DESC_TILED_TC4=128"],
+    "d": ["DESC_TILED_TR8=64", "DESC_TILED_TC8=128", "DESC_TILED_TR4=32", "DESC_TILED_TC4=64"],
+}
+out_dir = os.path.join(B.ROOT, "build_variants")
+os.makedirs(out_dir, exist_ok=True)
+with ThreadPoolExecutor(len(VARIANTS)) as ex:
+    for name, p in zip(VARIANTS, ex.map(lambda kv: B.build(defines=kv[1], out=os.path.join(out_dir, f"lib_tiled_{kv[0]}.so")), VARIANTS.items())):
+        print(name, p)

@@ -88,11 +88,11 @@ def run_case(batch, rows, cols, es, kernel="auto", ld_in=None, ld_out=None, stri
     return sel
 
 
-KERNELS = ["auto", "smem", "tma", "tma_st"]
+KERNELS = ["auto", "smem", "tiled", "tma", "tma_st"]
 
 
 def _kernels_for(es, rows, cols, ld_in, ld_out):
-    ks = ["auto", "smem"]
+    ks = ["auto", "smem", "tiled"]
     if (ld_in * es) % 16 == 0 and (ld_out * es) % 16 == 0:
         ks.append("tma")
         if es in (4, 8) and rows * es >= 16:
@@ -128,23 +128,26 @@ def test_edge_set(es, n):
 
 @pytest.mark.parametrize("es", [4, 8])
 def test_tight_ld_odd_shapes_fall_back(es):
-    """Tight ld that is not a 16-byte multiple: AUTO must pick the SMEM kernel and be exact."""
-    assert run_case(1, 67, 131, es) == "smem"
-    assert run_case(1, 3, 5, es) == "smem"
+    """Tight ld that is not a 16-byte multiple: AUTO must pick the TILED kernel and be exact;
+    the paper-schedule SMEM kernel too."""
+    assert run_case(1, 67, 131, es) == "tiled"
+    assert run_case(1, 3, 5, es) == "tiled"
+    run_case(1, 67, 131, es, "smem")
+    run_case(1, 130, 197, es, "tiled")
 
 
 @pytest.mark.parametrize("es", [4, 8])
 def test_padded_ld_guard_bands(es):
     """T4: 67x131 with ld_in=136, ld_out=72: padding columns and guard bands untouched."""
-    for k in ("auto", "tma", "tma_st", "smem"):
+    for k in ("auto", "tma", "tma_st", "smem", "tiled"):
         run_case(1, 67, 131, es, k, ld_in=136, ld_out=72)
 
 
 @pytest.mark.parametrize("es", [4, 8])
 def test_misaligned_base(es):
-    """Base offsets that break 16-byte alignment route to the SMEM kernel and stay exact."""
-    assert run_case(1, 100, 200, es, in_off=es) == "smem"
-    assert run_case(1, 100, 200, es, out_off=es) == "smem"
+    """Base offsets that break 16-byte alignment route to the TILED kernel and stay exact."""
+    assert run_case(1, 100, 200, es, in_off=es) == "tiled"
+    assert run_case(1, 100, 200, es, out_off=es) == "tiled"
     for k in ("tma", "tma_st"):
         with pytest.raises(desc.DescError, match="DESC_ERR_KERNEL"):
             run_case(1, 100, 200, es, k, in_off=es, check=False)
@@ -154,10 +157,12 @@ def test_misaligned_base(es):
 def test_batched_odd_strides(es):
     """T7: 7 x (33 x 65) with strides that leave gaps; input strides overlapping allowed."""
     v = 16 // es
-    for k in ("auto", "smem", "tma", "tma_st"):
+    for k in ("auto", "smem", "tiled", "tma", "tma_st"):
         run_case(7, 33, 65, es, k, ld_in=65 + (-65) % v, ld_out=40, stride_in=33 * 72 + v,
                  stride_out=65 * 40 + 2 * v)
     run_case(5, 20, 24, es, "smem", ld_in=24, ld_out=20, stride_in=24 * 10, stride_out=480)
+    run_case(5, 20, 24, es, "tiled", ld_in=24, ld_out=20, stride_in=24 * 10, stride_out=480)
+    run_case(3, 70, 99, es, "tiled", ld_in=101, ld_out=71, stride_in=101 * 75, stride_out=71 * 99)
 
 
 def test_involution_and_determinism():
@@ -243,7 +248,7 @@ def test_config2_8192_f32_and_i32():
     a = synth.random_bits((1, 8192, 8192), 4, synth.BASE_SEED + 2)
     x = torch.from_numpy(a[0].view(np.int32)).cuda()
     ref = oracle.transpose(a[0])
-    for k in ("auto", "tma", "tma_st", "smem"):
+    for k in ("auto", "tma", "tma_st", "smem", "tiled"):
         for dt in (torch.float32, torch.int32):
             y = desc.transpose(x.view(dt), kernel=k)
             torch.cuda.synchronize()
@@ -252,8 +257,9 @@ def test_config2_8192_f32_and_i32():
 
 def test_config3_3000x5000_f64_and_misaligned_ld():
     a = synth.random_bits((1, 3000, 5000), 8, synth.BASE_SEED + 3)
-    assert run_case(1, 3000, 5000, 8, src=a) == "tma_st"
-    assert run_case(1, 3000, 5000, 8, ld_in=5001, src=a) == "smem"
+    assert run_case(1, 3000, 5000, 8, src=a) == "tiled"
+    assert run_case(1, 3000, 5000, 8, ld_in=5001, src=a) == "tiled"
+    run_case(1, 3000, 5000, 8, "smem", ld_in=5001, src=a)
 
 
 def test_config4_batched_256x1024sq_f32():
