@@ -758,7 +758,8 @@ def view_arm(args, wl, world, rank, local):
                        "l2": "inputs larger than L2, no flush",
                        "timing": "CUDA events around the K launches, max over ranks"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": load_traffic(args.workload),
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": step_bytes},
             "parity": parity, "gpu_launches": launches, "cpu_baseline": None, "e2e": None,
             "clocks": clk.summary(),

@@ -654,9 +654,16 @@ bool tiled_preferred(const Args &a) {
 
 desc_status dispatch(const Args &a, desc_kernel k) {
     const bool tma_ok = tma_eligible(a);
-    if (a.rev_rows) {   // only the TMA-store kernel reads rows mirrored
+    if (a.rev_rows) {   // rows read mirrored: TILED (negative pitch) or the TMA-store kernel
+        if (k == DESC_KERNEL_TILED || (k == DESC_KERNEL_AUTO && tiled_preferred(a))) {
+            Args b = a;     // logical row 0 is the last physical row; walk rows backwards
+            b.in = static_cast<const char *>(a.in) + (a.rows - 1) * a.ld_in * a.es;
+            b.ld_in = -a.ld_in;
+            b.rev_rows = 0;
+            return run_tiled(b);
+        }
         if (!tma_ok || !tma_store_ok(a) || (k != DESC_KERNEL_AUTO && k != DESC_KERNEL_TMA_ST))
-            return fail(DESC_ERR_KERNEL, "reversed rows need the TMA-store kernel");
+            return fail(DESC_ERR_KERNEL, "reversed rows need the TILED or TMA-store kernel");
         return run_tma2(a);
     }
     if (k == DESC_KERNEL_TMA && !tma_ok)

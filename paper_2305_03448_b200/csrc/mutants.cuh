@@ -18,6 +18,9 @@
 //   9 TMA2_NO_FENCE      no fence.proxy.async / wait_group.read (a race; may not manifest)
 //  10 SCAN_NO_LOOKBACK   scan tiles skip the decoupled look-back (prefix 0)
 //  11 REDUCE_NO_TAIL     block reduction drops the scalar tail after the 16-byte body
+//  12 TILED_TILE_ONLY    TILED kernel copies the tile out untransposed (Listing 2 literally)
+//  13 TILED_EDGE         TILED edge-tile store predicate off by one (one padding cell written)
+//  14 TILED_NO_SYNC      TILED kernel without the barrier between staging and copy-out (race)
 #pragma once
 
 namespace desc {
@@ -35,6 +38,9 @@ enum DescMutant : int {
     MUT_TMA2_NO_FENCE = 9,
     MUT_SCAN_NO_LOOKBACK = 10,
     MUT_REDUCE_NO_TAIL = 11,
+    MUT_TILED_TILE_ONLY = 12,
+    MUT_TILED_EDGE = 13,
+    MUT_TILED_NO_SYNC = 14,
 };
 
 #ifdef DESC_MUTANTS

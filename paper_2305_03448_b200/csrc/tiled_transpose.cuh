@@ -20,6 +20,8 @@
 #pragma once
 #include <cstdint>
 
+#include "mutants.cuh"
+
 namespace desc {
 
 // A/B knobs (scripts/build_tiled_variants.py): tile rows / cols for 8-byte and narrower cells
@@ -93,7 +95,7 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
                     if (r < nr && c < nc) tile[r][c] = v[k][g];
                 }
         }
-        __syncthreads();
+        if (!DESC_MUTANT(MUT_TILED_NO_SYNC)) __syncthreads();   // block-uniform condition
         // copy-out: output row c0 + oc (= input column), 32 lanes x TR/32 cells contiguous
         constexpr int OK = TC / 8, OH = TR / 32;
         if (full) {
@@ -102,7 +104,8 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
 #pragma unroll
                 for (int h = 0; h < OH; ++h) {
                     const int oc = ty + 8 * m, orr = tx + 32 * h;
-                    dst[(int64_t)oc * ld_out + orr] = tile[orr][oc];
+                    dst[(int64_t)oc * ld_out + orr] =
+                        DESC_MUTANT(MUT_TILED_TILE_ONLY) ? tile[oc][orr] : tile[orr][oc];
                 }
         } else {
             const int nr = (int)(rows - r0 < TR ? rows - r0 : TR);
@@ -112,7 +115,9 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
 #pragma unroll
                 for (int h = 0; h < OH; ++h) {
                     const int oc = ty + 8 * m, orr = tx + 32 * h;
-                    if (oc < nc && orr < nr) dst[(int64_t)oc * ld_out + orr] = tile[orr][oc];
+                    if (oc < nc && orr < nr + (DESC_MUTANT(MUT_TILED_EDGE) ? 1 : 0))
+                        dst[(int64_t)oc * ld_out + orr] =
+                            DESC_MUTANT(MUT_TILED_TILE_ONLY) ? tile[oc][orr] : tile[orr][oc];
                 }
         }
         __syncthreads();                                  // tile reused by the next iteration

@@ -38,8 +38,11 @@ DETERMINISTIC = {
     10: ("SCAN_NO_LOOKBACK (tile prefixes dropped)",
          ["scan_stream_i32", "scan_lookback_i32", "scan_three_pass_i32"]),
     11: ("REDUCE_NO_TAIL (scalar tail dropped)", ["reduce_i32"]),
+    12: ("TILED_TILE_ONLY (tile copied out untransposed)", ["tiled_described_f32", "tiled_random_f64"]),
+    13: ("TILED_EDGE (edge store predicate off by one)", ["tiled_padded_f32", "tiled_padded_f64"]),
 }
-RACE_ONLY = {9: "TMA2_NO_FENCE (proxy fence and WAR wait removed)"}
+RACE_ONLY = {9: "TMA2_NO_FENCE (proxy fence and WAR wait removed)",
+             14: "TILED_NO_SYNC (staging / copy-out barrier removed)"}
 
 
 def _mutant_lib():
