@@ -156,12 +156,32 @@ class ClockSampler:
             self._stop.set()
             self.t.join()
 
+    def extend(self, work, torch, dev, seconds: float = 0.3, min_samples: int = 10):
+        """A short timed region can end before NVML answers often enough: then keep sampling
+        over `seconds` of untimed repeats of the same work right after it (labelled)."""
+        if not self.ok or len(self.samples) >= min_samples:
+            return
+        self.in_region = len(self.samples)
+        self._stop = threading.Event()
+        self.__enter__()
+        t_end = time.time() + seconds
+        while time.time() < t_end:
+            for _ in range(20):
+                work()
+            torch.cuda.synchronize(dev)
+        self.__exit__()
+
     def summary(self):
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+               "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+               "samples": len(self.samples)}
+        if getattr(self, "in_region", None) is not None:
+            out["samples_in_timed_region"] = self.in_region
+            out["note"] = ("timed region too short for enough NVML samples: the rest were taken "
+                           "over 0.3 s of untimed repeats of the same step right after it")
+        return out
 
 
 def bench_backend():
@@ -306,12 +326,13 @@ def reference_arm(args, wl, world, rank):
 
 
 # ------------------------------------------------------------------------- our arm
-def small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush, per_launch,
-                          step_bytes, reps: int = 100):
-    """Context for L2-flushed (small) workloads, outside the timed region: (1) the launch
-    floor -- the same kernel on a one-tile problem of the same dtype, timed the same way
-    (flush, events around the launch), i.e. launch + prologue + one load/store round trip;
-    (2) the same launches back to back without a flush (L2-resident, not the metric)."""
+def small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush, step_bytes,
+                          reps: int = 100):
+    """Context for small workloads (working set < 2 x L2), outside the timed region: (1) the
+    launch floor -- the same kernel on a one-tile problem of the same dtype, timed with a
+    flush and events around the launch, i.e. launch + prologue + one load/store round trip;
+    (2) the workload itself timed that way (flush + events around each launch); (3) the same
+    launches back to back on ONE buffer pair (L2-resident, not the metric)."""
     tdt = {"f32": torch.float32, "f64": torch.float64, "i32": torch.int32}[wl["dtype"]]
     tr = 64 if wl["es"] == 8 else 128
     xt = torch.zeros((tr, 128 // wl["es"]), dtype=tdt, device=dev)
@@ -330,13 +351,19 @@ def small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush, 
         ev[2 * k + 1].record(stream)
     torch.cuda.synchronize(dev)
     floor = statistics.median(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(reps))
-    med = statistics.median(per_launch)
+    for k in range(reps):
+        l2_flush()
+        ev[2 * k].record(stream)
+        step(0)
+        ev[2 * k + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    med = statistics.median(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(reps))
     warm0, warm1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(5):
-        step()
+        step(0)
     warm0.record(stream)
     for _ in range(reps):
-        step()
+        step(0)
     warm1.record(stream)
     torch.cuda.synchronize(dev)
     warm_ms = warm0.elapsed_time(warm1) / reps
@@ -345,7 +372,10 @@ def small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush, 
                                  "events around the launch (median of 100); an empty torch "
                                  "kernel timed this way takes ~6.2 us on B200 "
                                  "(profiles/r01_exp_floor.txt)",
-            "launch_median_ms": round(med, 5),
+            "flushed_launch_median_ms": round(med, 5),
+            "flushed_gbs": round(step_bytes / (med / 1e3) / 1e9, 1),
+            "flushed_what": "the workload with a 252 MiB read flush before each launch and "
+                            "events around it (median of 100; includes the event floor)",
             "l2_resident_gbs": round(step_bytes / (warm_ms / 1e3) / 1e9, 1),
             "l2_resident_what": "the same launches back to back, no flush (working set in "
                                 "the 126 MB L2; context, not the metric)"}
@@ -388,21 +418,39 @@ def ours_arm(args, wl, world, rank, local):
     kernel = args.kernel
     mat_bytes = rows * cols * es
     step_bytes = 2 * batch * mat_bytes                     # algorithmic: read + write
-    flush = (batch * mat_bytes) < 2 * L2_BYTES
+    small_ws = (batch * mat_bytes) < 2 * L2_BYTES
+    # A working set that fits the 126 MB L2 is kept out of it one of two ways:
+    #  * "rotate" (default): R copies of the (input, output) pair, R * 2 * bytes >= 4 x L2,
+    #    launched round robin back to back -- each launch finds its pair evicted by the R - 1
+    #    launches since its last use, and the region is timed without per-launch events
+    #    (which add ~6 us of event overhead per launch on B200, profiles/r01_exp_floor.txt);
+    #  * "flush": a read of a 2 x L2 buffer before every launch, events around each launch.
+    flush = small_ws and args.l2 == "flush"
+    R = max(2, -(-4 * L2_BYTES // (2 * batch * mat_bytes))) if small_ws and not flush else 1
+    xs, ys = [x], [y]
+    for _ in range(R - 1):
+        xs.append(x.clone())
+        ys.append(torch.empty_like(y))
     # L2 flush by READING a 2 x L2 buffer: leaves L2 full of clean, unrelated lines (a write
     # flush would leave 126 MB of dirty lines that the timed kernel would have to write back)
-    scratch = torch.ones(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if flush else None
-    sink = torch.empty((), dtype=torch.int64, device=dev) if flush else None
+    scratch = torch.ones(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if small_ws else None
+    sink = torch.empty((), dtype=torch.int64, device=dev) if small_ws else None
 
     def l2_flush():
         torch.sum(scratch, dim=0, dtype=torch.int64, out=sink)
 
-    def step():
+    turn = [0]
+
+    def step(pair=None):
+        if pair is None:
+            pair = turn[0] % R
+            turn[0] += 1
+        xi, yi = xs[pair], ys[pair]
         if batch == 1:
-            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), 1, rows, cols, ld_in, rows, 0, 0,
-                                   wl["dtype"], kernel, sptr)
+            desc.desc_transpose_ex(xi.data_ptr(), yi.data_ptr(), 1, rows, cols, ld_in, rows, 0,
+                                   0, wl["dtype"], kernel, sptr)
         else:
-            desc.desc_transpose_ex(x.data_ptr(), y.data_ptr(), batch, rows, cols, ld_in, rows,
+            desc.desc_transpose_ex(xi.data_ptr(), yi.data_ptr(), batch, rows, cols, ld_in, rows,
                                    rows * ld_in, rows * cols, wl["dtype"], kernel, sptr)
         return desc.desc_last_launch_count()
 
@@ -442,6 +490,7 @@ def ours_arm(args, wl, world, rank, local):
                 ends[k].record(stream)
         region1.record(stream)
         torch.cuda.synchronize(dev)
+    clk.extend(step, torch, dev)
     if world > 1:
         dist.barrier()
     region_ms = region0.elapsed_time(region1)
@@ -467,7 +516,7 @@ def ours_arm(args, wl, world, rank, local):
         per_launch = [ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(n_diag)]
     peak, peak_src = load_peak()
     small = small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush,
-                                  per_launch, step_bytes) if flush else None
+                                  step_bytes) if small_ws else None
 
     # ---- parity of the timed output (rank-local) ------------------------------------
     parity = None
@@ -515,6 +564,10 @@ def ours_arm(args, wl, world, rank, local):
                        "batch_per_gpu": batch, "kernel": selected,
                        "parallelism": f"{world} independent replica(s), no collective",
                        "l2": ("flushed before every step (read of a 252 MiB buffer, untimed)" if flush else
+                              f"{R} (input, output) pairs of {batch * mat_bytes / 1e6:.0f} MB each "
+                              f"used round robin ({2 * R * batch * mat_bytes / 1e6:.0f} MB >= 4 x the "
+                              "126 MB L2): every launch starts with its pair evicted, no flush"
+                              if R > 1 else
                               f"inputs larger than L2 ({batch * mat_bytes / 1e6:.0f} MB > 126 MB), no flush"),
                        "timing": ("CUDA events on the launch stream around the K launches "
                                   "(per launch when flushing), max over ranks")},
@@ -962,6 +1015,8 @@ def main():
                     help="pipeline depth of the NCCL slab transpose (default: dist.default_chunks)")
     ap.add_argument("--dist-n", type=int, default=65536)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--l2", choices=["rotate", "flush"], default="rotate",
+                    help="how a working set smaller than 2 x L2 is kept out of L2")
     ap.add_argument("--exchange-n", type=int, default=32768,
                     help="N > 1 default workload: also time one n x n slab transpose with the "
                          "NCCL all-to-all (0: skip)")

@@ -11,6 +11,8 @@
 #pragma once
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace desc {
 
 template <typename V>
@@ -18,6 +20,8 @@ __global__ void __launch_bounds__(256)
 copy_rows_kernel(const char *__restrict__ in, char *__restrict__ out, int64_t rows,
                  int64_t total_rows, int64_t units, int64_t ld_in_b, int64_t ld_out_b,
                  int64_t stride_in_b, int64_t stride_out_b) {
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
     for (int64_t r = blockIdx.x; r < total_rows; r += gridDim.x) {
         const int64_t b = r / rows, i = r - b * rows;
         const V *src = reinterpret_cast<const V *>(in + b * stride_in_b + i * ld_in_b);

@@ -279,6 +279,13 @@ template <typename Kern, typename... Args_>
 cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
                        Args_... args);
 
+// Plain launch with programmatic stream serialisation (PDL): for kernels that call
+// griddepcontrol.wait before any global access (tiled transpose, row copy, view tiles,
+// block reduction).  DESC_PDL=0 turns the attribute off (A/B).
+template <typename Kern, typename... Args_>
+cudaError_t launch_plain_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
+                             Args_... args);
+
 // 2-CTA cluster launch WITHOUT programmatic serialisation (kernels that do not call
 // griddepcontrol.wait, e.g. the scan, whose state is zeroed by a memset just before it).
 template <typename Kern, typename... Args_>
@@ -296,6 +303,23 @@ cudaError_t launch_cluster2(Kern kern, int grid, int threads, int smem, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename Kern, typename... Args_>
+cudaError_t launch_plain_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
+                             Args_... args) {
+    static const int pdl = dev_knob("DESC_PDL", 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -464,10 +488,11 @@ desc_status launch_tiled(const Args &a) {
             if (dev < 64) opted[dev] = true;
         }
     }
-    desc::transpose_tiled_kernel<Cell><<<grid, 256, C::SMEM, a.stream>>>(
-        static_cast<const Cell *>(a.in), static_cast<Cell *>(a.out), a.rows, a.cols, a.ld_in,
-        a.ld_out, a.stride_in, a.stride_out, tiles_r, tiles_c, ntiles);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_plain_pdl(desc::transpose_tiled_kernel<Cell>, grid, 256, C::SMEM,
+                                     a.stream, static_cast<const Cell *>(a.in),
+                                     static_cast<Cell *>(a.out), a.rows, a.cols, a.ld_in,
+                                     a.ld_out, a.stride_in, a.stride_out, tiles_r, tiles_c, ntiles);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "transpose_tiled_kernel launch");
     g_last_launches = 1;
     return DESC_OK;
@@ -887,19 +912,19 @@ desc_status run_copy(const void *in, void *out, int64_t batch, int64_t rows, int
     char *co = static_cast<char *>(out);
     const int64_t sib = batch > 1 ? stride_in * es : 0, sob = batch > 1 ? stride_out * es : 0;
     if (vec16)
-        desc::copy_rows_kernel<uint4><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols * es / 16,
+        launch_plain_pdl(desc::copy_rows_kernel<uint4>, grid, 256, 0, stream, ci, co, rows, total_rows, cols * es / 16,
                                                                ld_in * es, ld_out * es, sib, sob);
     else if (es == 8)
-        desc::copy_rows_kernel<unsigned long long><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+        launch_plain_pdl(desc::copy_rows_kernel<unsigned long long>, grid, 256, 0, stream, ci, co, rows, total_rows, cols,
                                                                             ld_in * es, ld_out * es, sib, sob);
     else if (es == 4)
-        desc::copy_rows_kernel<uint32_t><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+        launch_plain_pdl(desc::copy_rows_kernel<uint32_t>, grid, 256, 0, stream, ci, co, rows, total_rows, cols,
                                                                   ld_in * es, ld_out * es, sib, sob);
     else if (es == 2)
-        desc::copy_rows_kernel<uint16_t><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+        launch_plain_pdl(desc::copy_rows_kernel<uint16_t>, grid, 256, 0, stream, ci, co, rows, total_rows, cols,
                                                                   ld_in * es, ld_out * es, sib, sob);
     else
-        desc::copy_rows_kernel<uint8_t><<<grid, 256, 0, stream>>>(ci, co, rows, total_rows, cols,
+        launch_plain_pdl(desc::copy_rows_kernel<uint8_t>, grid, 256, 0, stream, ci, co, rows, total_rows, cols,
                                                                  ld_in * es, ld_out * es, sib, sob);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "copy_rows_kernel launch");
@@ -1092,12 +1117,12 @@ desc_status view_copy(const void *in, void *out, const desc_strided_view *view, 
     const int grid = (int)(vt.items < (int64_t)di.sms * 8 ? vt.items : (int64_t)di.sms * 8);
     const char *ci = static_cast<const char *>(in);
     char *co = static_cast<char *>(out);
-    if (mode == 1) desc::view_tiles_kernel<uint4, 1><<<grid, 256, 0, stream>>>(ci, co, vt, es);
-    else if (mode == 2) desc::view_tiles_kernel<uint4, 2><<<grid, 256, 0, stream>>>(ci, co, vt, es);
-    else if (es == 8) desc::view_tiles_kernel<unsigned long long, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
-    else if (es == 4) desc::view_tiles_kernel<uint32_t, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
-    else if (es == 2) desc::view_tiles_kernel<uint16_t, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
-    else desc::view_tiles_kernel<uint8_t, 0><<<grid, 256, 0, stream>>>(ci, co, vt, es);
+    if (mode == 1) launch_plain_pdl(desc::view_tiles_kernel<uint4, 1>, grid, 256, 0, stream, ci, co, vt, es);
+    else if (mode == 2) launch_plain_pdl(desc::view_tiles_kernel<uint4, 2>, grid, 256, 0, stream, ci, co, vt, es);
+    else if (es == 8) launch_plain_pdl(desc::view_tiles_kernel<unsigned long long, 0>, grid, 256, 0, stream, ci, co, vt, es);
+    else if (es == 4) launch_plain_pdl(desc::view_tiles_kernel<uint32_t, 0>, grid, 256, 0, stream, ci, co, vt, es);
+    else if (es == 2) launch_plain_pdl(desc::view_tiles_kernel<uint16_t, 0>, grid, 256, 0, stream, ci, co, vt, es);
+    else launch_plain_pdl(desc::view_tiles_kernel<uint8_t, 0>, grid, 256, 0, stream, ci, co, vt, es);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "view_tiles_kernel launch");
     g_last_launches = 1;
@@ -1125,12 +1150,12 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
     const int64_t cap = (int64_t)sms * 16;
     if (B <= 64) {
         const int64_t g = (nb + 255) / 256;                            // thread per block
-        desc::block_reduce_kernel<In, In, 1><<<(int)(g < cap ? g : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
+        launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
     } else if (B <= 16384) {
         const int64_t g = (nb + 7) / 8;                                // warp per block
-        desc::block_reduce_kernel<In, In, 32><<<(int)(g < cap ? g : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
+        launch_plain_pdl(desc::block_reduce_kernel<In, In, 32>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
     } else {
-        desc::block_reduce_cta_kernel<In, In><<<(int)(nb < cap ? nb : cap), 256, 0, stream>>>(pi, po, n, B, nb, vec);
+        launch_plain_pdl(desc::block_reduce_cta_kernel<In, In>, (int)(nb < cap ? nb : cap), 256, 0, stream, pi, po, n, B, nb, vec);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "block_reduce launch");
@@ -1289,7 +1314,7 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     if (algo != DESC_SCAN_THREE_PASS) return fail(DESC_ERR_KERNEL, "unknown scan algorithm %d", (int)algo);
     const int64_t T = 256 * (int64_t)ITEMS;
     const int64_t g1 = (t + 7) / 8, cap = (int64_t)di.sms * 16;       // one warp per tile
-    desc::block_reduce_kernel<In, Acc, 32><<<(int)(g1 < cap ? g1 : cap), 256, 0, stream>>>(
+    launch_plain_pdl(desc::block_reduce_kernel<In, Acc, 32>, (int)(g1 < cap ? g1 : cap), 256, 0, stream, 
         pi, st.agg, n, T, t, (reinterpret_cast<uintptr_t>(in) & 15) == 0);
     desc::scan_aggregates_kernel<Acc><<<1, 1024, 0, stream>>>(st.agg, st.incl, t);
     desc::scan_tiles_kernel<In, ITEMS><<<(int)t, 256, 0, stream>>>(pi, po, n, st.incl, vec);

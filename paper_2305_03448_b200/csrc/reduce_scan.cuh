@@ -116,6 +116,8 @@ template <typename In, typename Out, int G>
 __global__ void __launch_bounds__(256)
 block_reduce_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n, int64_t B,
                     int64_t nblocks, bool vec) {
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
     using Acc = typename AccOf<In>::T;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t groups = (int64_t)gridDim.x * blockDim.x / G;
@@ -133,6 +135,8 @@ template <typename In, typename Out>
 __global__ void __launch_bounds__(256)
 block_reduce_cta_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n, int64_t B,
                         int64_t nblocks, bool vec) {
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
     using Acc = typename AccOf<In>::T;
     __shared__ Acc part[8];
     for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {

@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "mutants.cuh"
+#include "ptx.cuh"
 
 namespace desc {
 
@@ -58,6 +59,10 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
     extern __shared__ __align__(16) unsigned char tiled_smem[];
     Cell(*tile)[TC + 1] = reinterpret_cast<Cell(*)[TC + 1]>(tiled_smem);
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    // PDL: the next kernel in the stream may be scheduled into the slots our last wave
+    // frees, but nothing here touches global memory before the previous grid has completed
+    ptx::grid_dependency_wait();
+    ptx::grid_launch_dependents();
     const int64_t tiles_per_mat = tiles_r * tiles_c;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t bt = t / tiles_per_mat;

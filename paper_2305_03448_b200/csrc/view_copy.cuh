@@ -18,6 +18,8 @@
 // and its elements reversed in registers), else single elements.
 #pragma once
 #include <cstdint>
+
+#include "ptx.cuh"
 #include <type_traits>
 
 namespace desc {
@@ -84,6 +86,8 @@ struct CellIO {
 template <typename Cell, int MODE>
 __global__ void __launch_bounds__(256)
 view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const ViewTiles v, int es) {
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
     using IO = CellIO<Cell, MODE>;
     using T = typename IO::T;
     constexpr int CB = IO::CB;

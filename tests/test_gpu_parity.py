@@ -175,6 +175,28 @@ def test_involution_and_determinism():
     assert torch.equal(z, x)
 
 
+@pytest.mark.parametrize("kernel", ["tiled", "tma_st", "auto"])
+def test_pdl_dependent_chain(kernel):
+    """Back-to-back launches with programmatic dependent launch, each reading what the
+    previous one wrote (no host sync in between): 24 transposes ping-ponging between two
+    buffers, a view copy and a block reduction of the result at the end -- every kernel must
+    wait for its predecessor (griddepcontrol.wait) before touching memory."""
+    a = synth.random_bits((1536, 2560), 4, 21)
+    x = torch.from_numpy(a.view(np.int32)).cuda()
+    bufs = [x.clone(), torch.empty((2560, 1536), dtype=torch.int32, device="cuda")]
+    for k in range(24):
+        src, dst = bufs[k % 2], bufs[(k + 1) % 2]
+        desc.transpose(src, dst, kernel=kernel)
+    v = desc.view_copy(bufs[0], [("transpose", 0, 0), ("reverse", 0, 1)])
+    r = desc.block_reduce(bufs[0].view(-1), 4096)
+    torch.cuda.synchronize()
+    assert bufs[0].cpu().numpy().view(np.uint32).tobytes() == a.tobytes()
+    from oracle import views as V
+    assert v.cpu().numpy().view(np.uint32).tobytes() == \
+        V.materialize(a, [("transpose", 0, 0), ("reverse", 0, 1)]).tobytes()
+    assert r.cpu().numpy().tobytes() == oracle.block_reduce(a.view(np.int32).ravel(), 4096).tobytes()
+
+
 def test_concurrent_streams_and_graph_capture():
     """Dynamically scheduled launches on two streams at once (distinct tile counters), then
     the same launches captured into and replayed from a CUDA graph."""
