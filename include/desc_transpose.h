@@ -140,7 +140,10 @@ desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
  * The library streams row bands of the input through the caller-provided device
  * workspace d_work (256-byte aligned, work_bytes >= desc_transpose_host_workspace
  * recommended; smaller works down to one row): H2D copy of band k+1, transpose of
- * band k and D2H copy of band k-1 overlap on two internal streams.  Asynchronous on
+ * band k and D2H copy of band k-1 overlap on two internal streams.  When that would
+ * take more than 64 bands (e.g. many small batched matrices) and both host buffers are
+ * page-locked and mapped, one TILED kernel instead reads and writes the host buffers
+ * directly over PCIe (zero-copy; d_work is then unused).  Asynchronous on
  * `stream` like the device entry points: the host buffers must stay valid and
  * untouched until the stream reaches the end of the operation.  h_in/h_out that are
  * device memory give DESC_ERR_MEMSPACE; a too-small workspace gives DESC_ERR_SHAPE. */

@@ -792,6 +792,18 @@ desc_status check_host_ptr(const void *p, const char *name) {
     return DESC_OK;
 }
 
+// Page-locked host memory mapped into the device address space: its device pointer.
+bool mapped_host(const void *p, void **dptr) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (attr.type != cudaMemoryTypeHost || attr.devicePointer == nullptr) return false;
+    *dptr = attr.devicePointer;
+    return true;
+}
+
 desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows, int64_t cols,
                      int64_t ld_in, int64_t ld_out, int64_t stride_in, int64_t stride_out, int es,
                      void *d_work, size_t work_bytes, cudaStream_t stream) {
@@ -828,6 +840,24 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     if (band_bytes(band, cols, es) > (int64_t)work_bytes)
         return fail(DESC_ERR_SHAPE, "d_work (%zu bytes) too small: need >= %lld", work_bytes,
                     (long long)band_bytes(1, cols, es));
+
+    // Zero-copy mode: when both host buffers are page-locked and mapped, the TILED kernel
+    // reads the input and writes the transposed output straight over PCIe in one pass.
+    // SM loads / stores reach 51 / 53 GB/s per direction and 80 GB/s both ways at once
+    // against the copy engines' 56 / 57 / 99.5 (scripts/exp_zerocopy.cu,
+    // profiles/r01_exp_zerocopy.txt), so AUTO keeps the banded copy pipeline unless it
+    // would be cut into many small copies (> 64 bands, e.g. 256 x 1024^2: 62 GB/s banded vs
+    // 75 GB/s zero-copy).  DESC_HOST_MODE=1 forces bands, =2 forces zero-copy (A/B).
+    static const int host_mode = dev_knob("DESC_HOST_MODE", 0);
+    const int64_t nbands = batch * ((rows + band - 1) / band);
+    void *dz_in = nullptr, *dz_out = nullptr;
+    if ((host_mode == 2 || (host_mode == 0 && nbands > 64)) && mapped_host(h_in, &dz_in) &&
+        mapped_host(h_out, &dz_out)) {
+        Args a{dz_in, dz_out, batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, stream};
+        if (desc_status st = run_tiled(a)) return st;
+        g_last_launches = 1;
+        return DESC_OK;
+    }
 
     HostPipe *hp;
     if (desc_status s = host_pipe(dev, &hp)) return s;

@@ -336,6 +336,22 @@ def test_transpose_host_bands(pinned):
             assert got.tobytes() == oracle.transpose(src if batch > 1 else src[0]).tobytes()
 
 
+def test_transpose_host_zero_copy_many_bands():
+    """> 64 bands with pinned (mapped) host buffers: one TILED launch over PCIe reads and
+    writes the host buffers directly; pageable buffers keep the banded copy pipeline."""
+    src = synth.random_bits((80, 70, 50), 4, 123)
+    for pinned in (True, False):
+        x = torch.from_numpy(src.view(np.int32))
+        if pinned:
+            x = x.pin_memory()
+        nbytes = desc.desc_transpose_host_workspace(64, 50, "i32")
+        work = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        y = desc.transpose_host(x, work=work)
+        torch.cuda.synchronize()
+        assert desc.desc_last_launch_count() == (1 if pinned else 160)
+        assert y.numpy().view(np.uint32).tobytes() == oracle.transpose(src).tobytes()
+
+
 def test_transpose_host_rejects_device_buffers():
     d = torch.empty((64, 64), dtype=torch.float32, device="cuda")
     work = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
