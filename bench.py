@@ -80,6 +80,7 @@ WORKLOADS["scan64M_f32"] = dict(batch=1, rows=1, cols=1 << 26, dtype="f32", es=4
                                 name="inclusive scan, n = 2^26 f32 (256 MB) (SURVEY 8(f) NEXT #4, P:1047)")
 WORKLOADS["scan64M_i32"] = dict(batch=1, rows=1, cols=1 << 26, dtype="i32", es=4, op="scan",
                                 name="inclusive scan, n = 2^26 i32 (256 MB) (SURVEY 8(f) NEXT #4, P:1047)")
+NOMINAL_HBM_GBS = 8000.0  # BASELINE.json north star / SURVEY 8(d): the nominal B200 HBM3e figure
 NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU
 
 
@@ -573,6 +574,8 @@ def ours_arm(args, wl, world, rank, local):
                                   "(per launch when flushing), max over ranks")},
             "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "nominal_peak": NOMINAL_HBM_GBS,
+                         "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(args.workload), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes,
@@ -811,6 +814,8 @@ def view_arm(args, wl, world, rank, local):
                        "l2": "inputs larger than L2, no flush",
                        "timing": "CUDA events around the K launches, max over ranks"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "nominal_peak": NOMINAL_HBM_GBS,
+                         "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(args.workload),
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": step_bytes},
@@ -910,6 +915,8 @@ def op_arm(args, wl, world, rank, local):
                        "l2": "inputs larger than L2, no flush",
                        "timing": "CUDA events around the K launches, max over ranks"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "nominal_peak": NOMINAL_HBM_GBS,
+                         "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                          "peak_source": peak_src + ("; read-only stream, may exceed a copy's "
                                                     "read+write rate" if op == "reduce" else ""),
