@@ -230,13 +230,13 @@ desc_status desc_block_reduce(const void *in, void *out, int64_t n, int64_t bloc
 
 /* Inclusive scan: out[i] = sum(in[0..i]), same dtypes and arithmetic as desc_block_reduce.
  * Needs a device workspace of desc_scan_workspace(n, dtype) bytes, 256-byte aligned (tile
- * status; zeroed by the call with cudaMemsetAsync on `stream`), else DESC_ERR_SHAPE.  in ==
+ * status; zeroed by the call with a reset kernel on `stream`), else DESC_ERR_SHAPE.  in ==
  * out (in place) is allowed; partial overlap gives DESC_ERR_ALIAS.
  * Algorithms (desc_scan_ex; desc_scan = AUTO):
- *   DESC_SCAN_LOOKBACK  : one launch, one 8-32 KB tile per CTA, decoupled look-back.
+ *   DESC_SCAN_LOOKBACK  : state reset + one launch, one 8-32 KB tile per CTA, decoupled look-back.
  *   DESC_SCAN_THREE_PASS: tile aggregates -> aggregate scan -> tile scans (3 launches,
  *                         3 n bytes of traffic; the paper's multi-kernel shape).
- *   DESC_SCAN_STREAM    : one launch, persistent CTAs stream 96 KB tiles through a
+ *   DESC_SCAN_STREAM    : state reset + one launch, persistent CTAs stream 96 KB tiles through a
  *                         shared-memory ring (1-D TMA bulk copies) with a coalesced
  *                         look-back; 2 n bytes.  Needs 16-byte aligned in and out.
  * AUTO takes STREAM for aligned arrays of >= 2 tiles per SM, LOOKBACK for shorter ones,

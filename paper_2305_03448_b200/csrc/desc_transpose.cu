@@ -1268,6 +1268,17 @@ template <int ES>
 using ScanStreamC = desc::ScanStreamCfg<kScanNR, scan_vpt(ES), scan_stages(ES),
                                         DESC_SCAN_TMEM_SLOTS, DESC_SCAN_LB_WARPS>;
 
+// zero `bytes` (a multiple of 16) of scan state in stream order, PDL-chained
+desc_status scan_reset(char *work, int64_t bytes, const DevInfo &di, cudaStream_t stream) {
+    const int64_t n16 = bytes / 16;
+    const int64_t want = (n16 + 255) / 256, cap = (int64_t)di.sms * 4;
+    cudaError_t e = launch_plain_pdl(desc::scan_reset_kernel, (int)(want < cap ? want : cap), 256,
+                                     0, stream, reinterpret_cast<uint4 *>(work), n16);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "scan_reset launch");
+    return DESC_OK;
+}
+
 template <typename In, int ITEMS>
 desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool vec,
                         desc_scan_algo algo, cudaStream_t stream) {
@@ -1313,8 +1324,8 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute (scan)");
         st.dhi = reinterpret_cast<uint64_t *>(work + 256 + round_up(ts * 8, 256));
-        e = cudaMemsetAsync(work, 0, 256 + desc_words * round_up(ts * 8, 256), stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (scan state)");
+        if (desc_status s = scan_reset(work, 256 + desc_words * round_up(ts * 8, 256), di, stream))
+            return s;
         const int64_t grid = ts < di.sms ? ts : di.sms;
         // TMA view of the input: rows of 128 bytes (the < 128-byte tail is read directly)
         const int64_t bulk_rows = n * es / 128;
@@ -1325,20 +1336,21 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
                      128 / es, SC::BOX_ROWS};
             if (desc_status s = tensor_map(k, &map)) return s;
         }
-        e = launch_cluster2(kern, (int)grid, SC::THREADS, smem, stream, map, pi, po, n, ts,
-                            bulk_rows, st);
+        e = launch_pdl(kern, (int)grid, SC::THREADS, smem, stream, map, pi, po, n, ts, bulk_rows,
+                       st);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "scan_stream launch");
-        g_last_launches = 1;
+        g_last_launches = 2;
         return DESC_OK;
     }
     if (algo == DESC_SCAN_LOOKBACK) {
-        e = cudaMemsetAsync(work, 0, 256 + desc_words * round_up(t * 8, 256), stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (scan state)");
-        desc::scan_kernel<In, In, ITEMS><<<(int)t, 256, 0, stream>>>(pi, po, n, st, vec);
-        e = cudaGetLastError();
+        if (desc_status s = scan_reset(work, 256 + desc_words * round_up(t * 8, 256), di, stream))
+            return s;
+        e = launch_plain_pdl(desc::scan_kernel<In, In, ITEMS>, (int)t, 256, 0, stream, pi, po, n,
+                             st, vec);
+        if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "scan launch");
-        g_last_launches = 1;
+        g_last_launches = 2;
         return DESC_OK;
     }
     if (algo != DESC_SCAN_THREE_PASS) return fail(DESC_ERR_KERNEL, "unknown scan algorithm %d", (int)algo);

@@ -348,6 +348,16 @@ __device__ __forceinline__ void set_elem(uint4 &v, int j, In e) {
 // The tile's elements stay packed in 16-byte registers (ITEMS * sizeof(In) / 16 of them):
 // half the registers of an accumulator-typed copy for f32 -> more resident tiles per SM,
 // which is what hides the look-back latency.
+// Zeroes the single-pass scans' state (tile counter + descriptors) in stream order; a kernel
+// rather than cudaMemsetAsync so that it and the scan after it chain with PDL.
+__global__ void __launch_bounds__(256) scan_reset_kernel(uint4 *__restrict__ p, int64_t n16) {
+    ptx::grid_dependency_wait();
+    ptx::grid_launch_dependents();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4(0, 0, 0, 0);
+}
+
 template <typename In, typename Out, int ITEMS>
 __global__ void __launch_bounds__(256, 4)
 scan_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
@@ -357,6 +367,8 @@ scan_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
     constexpr int V = 16 / sizeof(In);
     constexpr int NV = ITEMS / V;
     static_assert(sizeof(In) == sizeof(Out), "scan output has the input's type");
+    ptx::grid_dependency_wait();       // PDL: the state reset (and anything before) is done
+    ptx::grid_launch_dependents();
     __shared__ Acc warp_tot[8];
     __shared__ Acc tile_prefix;
     __shared__ uint32_t tile_s;
@@ -636,6 +648,8 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
     __shared__ __align__(8) uint64_t tpre[Q];                    // exclusive prefix
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    ptx::grid_dependency_wait();       // PDL: the state reset (and anything before) is done
+    ptx::grid_launch_dependents();
 
     if (tid == 0) {
 #pragma unroll
