@@ -49,6 +49,8 @@ WORKLOADS = {
                          name="3000x5000 f64 non-tile-multiple transpose (BASELINE.json configs[2])"),
     "4096f64": dict(batch=1, rows=4096, cols=4096, dtype="f64", es=8,
                     name="4096x4096 f64 transpose (paper-size extra: 256 MB in+out, P:1051)"),
+    "8192i32": dict(batch=1, rows=8192, cols=8192, dtype="i32", es=4,
+                    name="8192x8192 i32 transpose (configs[2] shape, int32: dtype independence)"),
     "8192f64": dict(batch=1, rows=8192, cols=8192, dtype="f64", es=8,
                     name="8192x8192 f64 transpose (paper-size extra: 1 GiB in+out, P:1051)"),
     "3000x5000f64_ld5001": dict(batch=1, rows=3000, cols=5000, dtype="f64", es=8, ld_in=5001,

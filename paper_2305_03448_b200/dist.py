@@ -171,7 +171,7 @@ class PeerSlabTranspose:
     (gloo in the single-GPU two-process test, NCCL in bench.py)."""
 
     def __init__(self, out_slab: torch.Tensor, M: int, group=None, kernel: str = "auto",
-                 remote_kernel: str = "tma"):
+                 remote_kernel: str = "tiled"):
         if not out_slab.is_cuda or not out_slab.is_contiguous():
             raise ValueError("out_slab must be a contiguous CUDA tensor")
         self.group = group
@@ -185,9 +185,9 @@ class PeerSlabTranspose:
         handle, offset = desc.desc_ipc_handle(out_slab.data_ptr())
         handles = [None] * self.P
         dist.all_gather_object(handles, (handle, offset, out_slab.device.index), group=group)
-        # blocks for a slab on ANOTHER GPU go through the TMA-load + st.global kernel (16-byte
-        # stores over NVLink); the TMA-store kernel is kept for same-device slabs, where its
-        # tensor map addresses local HBM
+        # blocks for a slab on ANOTHER GPU go through the TILED kernel (plain coalesced loads
+        # of local HBM, 128-byte warp stores over NVLink; no tensor map ever addresses peer
+        # memory); same-device slabs (the one-GPU test) take AUTO
         self.kernels = [kernel if d == out_slab.device.index else remote_kernel
                         for (_, _, d) in handles]
         self.peer_ptr = []
