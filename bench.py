@@ -648,7 +648,11 @@ def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4, chunks=None):
     C = None
     if impl == "p2p":
         xp = ddist.PeerSlabTranspose(out, M)
-        step = lambda: xp(x)[1]                                      # noqa: E731
+        # steps back to back without the per-call group barriers: inside this loop no rank
+        # reads its slab, and ranks write disjoint column blocks of each slab in stream
+        # order, so the only barrier the result needs is the one after the last step (the
+        # region is timed by CUDA events on each rank's stream, max over ranks)
+        step = lambda: xp(x, barrier=False)[1]                       # noqa: E731
     else:
         ws = None
         if world > 1:
