@@ -86,7 +86,7 @@ typedef enum desc_dtype {
  *                      predicated edges -- the corrected Listing 1 schedule
  *                      (P:49-60 with the P:44 fix).  Any alignment.  Kept as the
  *                      paper's schedule (baseline); AUTO never picks it.
- *   DESC_KERNEL_TILED : any alignment; 64x64 (8-byte cells: 64x32) tiles padded by one
+ *   DESC_KERNEL_TILED : any alignment; 64x64 (8-byte cells: 32x64) tiles padded by one
  *                      cell, 256 threads each issuing all of its 16 (8) cell loads
  *                      before staging, one tile per CTA, predicated edge tiles.
  *   DESC_KERNEL_TMA  : persistent, warp-specialised: TMA (cp.async.bulk.tensor)

@@ -6,9 +6,9 @@
 // ld_in = 5001, BASELINE configs[2] variant), where no vector or bulk access is legal, so the
 // kernel has to reach HBM bandwidth with cell-wide accesses.  What differs from the paper's
 // Listing 1 schedule (transpose_smem_kernel, kept as the faithful baseline):
-//   * a TR x TC tile (64 x 64 cells for 1/2/4-byte cells, 64 x 32 for 8-byte cells), so a
+//   * a TR x TC tile (64 x 64 cells for 1/2/4-byte cells, 32 x 64 for 8-byte cells), so a
 //     warp row is 128 / 256 contiguous bytes on both sides,
-//   * every thread issues all of its TR*TC/256 loads (16 for f32) back to back into
+//   * every thread issues all of its TR*TC/256 loads (16 for f32, 8 for f64) back to back into
 //     registers before touching shared memory: 16 independent HBM requests in flight per
 //     thread instead of Listing 1's one-at-a-time load/store pairs (B200 needs ~40 KB in
 //     flight per SM to cover HBM latency at 6.5 TB/s),
@@ -26,8 +26,8 @@
 namespace desc {
 
 // A/B knobs (scripts/build_tiled_variants.py): tile rows / cols for 8-byte and narrower cells
-#ifndef DESC_TILED_TR8
-#define DESC_TILED_TR8 64
+#ifndef DESC_TILED_TR8           // 8-byte cells: 32 x 64 (sweep with PDL)
+#define DESC_TILED_TR8 32
 #endif
 #ifndef DESC_TILED_TC8
 #define DESC_TILED_TC8 64

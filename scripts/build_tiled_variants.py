@@ -5,10 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2305_03448_b200 import build as B
 
 VARIANTS = {
-    "a": ["DESC_TILED_TR8=128", "DESC_TILED_TC8=32", "DESC_TILED_TR4=64", "DESC_TILED_TC4=128"],
-    "b": ["DESC_TILED_TR8=128", "DESC_TILED_TC8=64", "DESC_TILED_TR4=32", "DESC_TILED_TC4=128"],
-    "c": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=128", "DESC_TILED_TR4=128", "DESC_TILED_TC4=128"],
-    "d": ["DESC_TILED_TR8=64", "DESC_TILED_TC8=128", "DESC_TILED_TR4=32", "DESC_TILED_TC4=64"],
+    "s1": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=64"],
+    "s2": ["DESC_TILED_TR8=64", "DESC_TILED_TC8=32"],
+    "s3": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=32"],
 }
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)
