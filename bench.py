@@ -82,6 +82,8 @@ WORKLOADS["scan64M_f32"] = dict(batch=1, rows=1, cols=1 << 26, dtype="f32", es=4
                                 name="inclusive scan, n = 2^26 f32 (256 MB) (SURVEY 8(f) NEXT #4, P:1047)")
 WORKLOADS["scan64M_i32"] = dict(batch=1, rows=1, cols=1 << 26, dtype="i32", es=4, op="scan",
                                 name="inclusive scan, n = 2^26 i32 (256 MB) (SURVEY 8(f) NEXT #4, P:1047)")
+WORKLOADS["scan32M_f64"] = dict(batch=1, rows=1, cols=1 << 25, dtype="f64", es=8, op="scan",
+                                name="inclusive scan, n = 2^25 f64 (256 MB) (SURVEY 8(f) NEXT #4, P:1047)")
 NOMINAL_HBM_GBS = 8000.0  # BASELINE.json north star / SURVEY 8(d): the nominal B200 HBM3e figure
 NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU
 
@@ -848,8 +850,8 @@ def op_arm(args, wl, world, rank, local):
     if world > 1:
         init_pg(dev)
     n, es, op = wl["cols"], wl["es"], wl["op"]
-    npdt = {"f32": np.float32, "i32": np.int32}[wl["dtype"]]
-    a = (synth.random_floats(n, npdt, synth.BASE_SEED + 11 + rank) if npdt == np.float32
+    npdt = {"f32": np.float32, "f64": np.float64, "i32": np.int32}[wl["dtype"]]
+    a = (synth.random_floats(n, npdt, synth.BASE_SEED + 11 + rank) if npdt != np.int32
          else synth.random_ints(n, npdt, synth.BASE_SEED + 11 + rank))
     x = torch.from_numpy(a).to(dev)
     stream = torch.cuda.current_stream(dev)
@@ -901,8 +903,8 @@ def op_arm(args, wl, world, rank, local):
             ref = oracle.scan(a)
             absx = oracle.scan(np.abs(a).astype(np.float64))
             m = np.arange(1, n + 1)
-        if npdt == np.float32:
-            tol = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64) + \
+        if npdt != np.int32:
+            tol = np.spacing(np.abs(ref).astype(npdt)).astype(np.float64) + \
                 2.0 * m * 2.0 ** -53 * absx
             ok = bool(np.all(np.abs(got.astype(np.float64) - ref) <= tol))
             parity = ("within the fp summation-order bound vs oracle" if ok else "MISMATCH")

@@ -1246,9 +1246,16 @@ int64_t scan_workspace_bytes(int64_t n, int es) {
     return 256 + (single > three ? single : three);
 }
 
-// streaming scan: 8 reduce + 8 scan warps, tiles of 8 x 32 lanes x 12 16-byte vectors =
-// 48 KB, a 4-stage shared-memory ring (192 KB), 5 tiles (5 x 96 columns) parked in TMEM
-#ifndef DESC_SCAN_VPT        // compile-time overrides: A/B builds only
+// streaming scan: NR reduce + NR scan warps, tiles of NR x 32 lanes x VPT 16-byte vectors,
+// an S-stage shared-memory ring, QT tiles parked in TMEM.  Per element type (A/B sweeps in
+// profiles/r01_scan_sweeps.txt, fraction of the measured peak):
+//   4-byte integers : 8 + 8 warps x 12 vectors (48 KB tiles), 4 stages, 5 slots   i32 0.91
+//   f32 (f64 sums)  : 12 + 12 warps x 8 vectors (48 KB), 4 stages, 5 slots       f32 0.843 -> 0.86
+//   f64 / 64-bit    : 12 + 12 warps x 10 vectors (60 KB), 3 stages, 4 slots      f64 0.924 -> 0.934
+// With 8-byte accumulators every warp-scan level is two shuffles and the adds are f64, so
+// the scan warps are the slower side: more warps in flight and shorter per-warp carry
+// chains pay there, while the same split costs i32 0.905 -> 0.893.
+#ifndef DESC_SCAN_VPT        // compile-time overrides of the 4-byte integer path: A/B builds
 #define DESC_SCAN_VPT 12
 #endif
 #ifndef DESC_SCAN_STAGES
@@ -1260,13 +1267,23 @@ int64_t scan_workspace_bytes(int64_t n, int es) {
 #ifndef DESC_SCAN_LB_WARPS
 #define DESC_SCAN_LB_WARPS 1
 #endif
-// (bytes: 6 vectors per lane -- 16 elements per vector -- in 8 stages)
-constexpr int kScanNR = 8;
-constexpr int scan_vpt(int es) { return es == 1 ? 6 : DESC_SCAN_VPT; }
-constexpr int scan_stages(int es) { return es == 1 ? 8 : DESC_SCAN_STAGES; }
-template <int ES>
-using ScanStreamC = desc::ScanStreamCfg<kScanNR, scan_vpt(ES), scan_stages(ES),
-                                        DESC_SCAN_TMEM_SLOTS, DESC_SCAN_LB_WARPS>;
+template <typename In> struct ScanPick {       // 4-byte integers
+    static constexpr int NR = 8, VPT = DESC_SCAN_VPT, S = DESC_SCAN_STAGES,
+                         QT = DESC_SCAN_TMEM_SLOTS;
+};
+template <> struct ScanPick<uint8_t> {         // 6 vectors per lane (16 elements each), 8 stages
+    static constexpr int NR = 8, VPT = 6, S = 8, QT = DESC_SCAN_TMEM_SLOTS;
+};
+template <> struct ScanPick<float> {
+    static constexpr int NR = 12, VPT = 8, S = 4, QT = 5;
+};
+template <> struct ScanPick<double> {
+    static constexpr int NR = 12, VPT = 10, S = 3, QT = 4;
+};
+template <> struct ScanPick<uint64_t> : ScanPick<double> {};
+template <typename In>
+using ScanStreamC = desc::ScanStreamCfg<ScanPick<In>::NR, ScanPick<In>::VPT, ScanPick<In>::S,
+                                        ScanPick<In>::QT, DESC_SCAN_LB_WARPS>;
 
 // zero `bytes` (a multiple of 16) of scan state in stream order, PDL-chained
 desc_status scan_reset(char *work, int64_t bytes, const DevInfo &di, cudaStream_t stream) {
@@ -1306,7 +1323,8 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     if (desc_status s = device_info(dev, &di)) return s;
     // streaming tiles (96 KB) are never more than the look-back tiles (<= 32 KB), so the
     // workspace sized by scan_tiles() covers both
-    using SC = ScanStreamC<(int)sizeof(In)>;
+    using SP = ScanPick<In>;
+    using SC = ScanStreamC<In>;
     constexpr int64_t TBY = SC::TB;
     const int64_t ts = (n * es + TBY - 1) / TBY;
     if (algo == DESC_SCAN_AUTO) {
@@ -1317,8 +1335,7 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     }
     if (algo == DESC_SCAN_STREAM) {
         if (!vec) return fail(DESC_ERR_KERNEL, "streaming scan needs 16-byte aligned in and out");
-        auto kern = desc::scan_stream_kernel<In, kScanNR, scan_vpt(sizeof(In)),
-                                             scan_stages(sizeof(In)), DESC_SCAN_TMEM_SLOTS,
+        auto kern = desc::scan_stream_kernel<In, SP::NR, SP::VPT, SP::S, SP::QT,
                                              DESC_SCAN_LB_WARPS>;
         const int smem = SC::SMEM;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -98,15 +98,19 @@ def main():
                   else y.cpu().numpy().tobytes() == ref.tobytes())
             bad += not ok
             print(f"scan {algo} {dt.__name__} n={n}: {'ok' if ok else 'MISMATCH'}", flush=True)
-    # streaming scan, several tiles per CTA (48 KB tiles: ~10 per CTA on 148 SMs)
-    n = 148 * 10 * 12288 + 5
-    a = synth.random_ints(n, np.int32, 6)
-    x = torch.from_numpy(a).cuda()
-    y = desc.scan(x, algo="stream")
-    torch.cuda.synchronize()
-    ok = y.cpu().numpy().tobytes() == oracle.scan(a).tobytes()
-    bad += not ok
-    print(f"scan stream int32 n={n}: {'ok' if ok else 'MISMATCH'}", flush=True)
+    # streaming scan, several tiles per CTA so every stage ring and TMEM slot ring wraps
+    # (i32 48 KB tiles ~10 per CTA; f32 48 KB tiles ~6; f64 60 KB tiles ~5, on 148 SMs)
+    for dt, n in ((np.int32, 148 * 10 * 12288 + 5), (np.float32, 148 * 6 * 12288 + 7),
+                  (np.float64, 148 * 5 * 7680 + 3)):
+        a = (synth.random_ints(n, dt, 6) if dt == np.int32 else synth.random_floats(n, dt, 6))
+        x = torch.from_numpy(a).cuda()
+        y = desc.scan(x, algo="stream")
+        torch.cuda.synchronize()
+        ref = oracle.scan(a)
+        ok = (y.cpu().numpy().tobytes() == ref.tobytes() if dt == np.int32
+              else np.allclose(y.cpu().numpy(), ref, rtol=1e-5, atol=1e-3))
+        bad += not ok
+        print(f"scan stream {dt.__name__} n={n}: {'ok' if ok else 'MISMATCH'}", flush=True)
     print("sanitize driver:", "PASS" if bad == 0 else f"{bad} FAILURES")
     return 1 if bad else 0
 
