@@ -275,6 +275,28 @@ void sched_lookup(int dev, cudaStream_t stream, unsigned long long **out) {
 // Launch with programmatic stream serialisation (PDL) so that back-to-back transposes
 // overlap launch latency and prologue with the previous kernel's tail; the kernels call
 // griddepcontrol.wait before touching global memory, so stream order is preserved.
+// cluster launch (cluster size `cl`, grid a multiple of it) with programmatic serialisation
+template <typename Kern, typename... Args_>
+cudaError_t launch_cluster_pdl(Kern kern, int grid, int cl, int threads, int smem,
+                               cudaStream_t stream, Args_... args) {
+    static const int pdl = dev_knob("DESC_PDL", 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename Kern, typename... Args_>
 cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t stream,
                        Args_... args);
@@ -1175,17 +1197,42 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
                           int sms, cudaStream_t stream) {
     const In *pi = static_cast<const In *>(in);
     In *po = static_cast<In *>(out);
-    // grid: up to 16 x 256-thread CTAs per SM, grid-striding over the blocks (measured best
-    // against balanced-round and one-block-per-group grids: 0.855 vs 0.834 / 0.833)
-    const int64_t cap = (int64_t)sms * 16;
+    // grid: one wave of 8 x 256-thread CTAs per SM, grid-striding over the blocks, 8 16-byte
+    // loads in flight per lane (2^26 f32, B = 1024: 0.966 of peak; the earlier 16 CTAs/SM
+    // with 4 loads in flight 0.89; profiles/r01_reduce_sweep.txt)
+#ifndef DESC_REDUCE_CTAS_PER_SM
+#define DESC_REDUCE_CTAS_PER_SM 8
+#endif
+#ifndef DESC_REDUCE_ROWS
+#define DESC_REDUCE_ROWS 1
+#endif
+    const int64_t cap = (int64_t)sms * DESC_REDUCE_CTAS_PER_SM;
     if (B <= 64) {
         const int64_t g = (nb + 255) / 256;                            // thread per block
         launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
+    } else if (vec && n % B == 0 && (B * (int64_t)sizeof(In)) % 512 == 0 &&
+               B * (int64_t)sizeof(In) <= 2048 && DESC_REDUCE_ROWS) {
+        // whole blocks of 1, 2 or 4 warp rows (the ragged-tail-free case; others below)
+        const int64_t P = B * (int64_t)sizeof(In) / 512, g = (nb * P / 8 + 7) / 8 + 1;
+        const int grid = (int)(g < 2 * cap ? g : 2 * cap);   // 16 CTAs/SM measured best here
+        if (P == 1) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 1>, grid, 256, 0, stream, pi, po, nb);
+        else if (P == 2) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 2>, grid, 256, 0, stream, pi, po, nb);
+        else launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 4>, grid, 256, 0, stream, pi, po, nb);
     } else if (B <= 16384) {
         const int64_t g = (nb + 7) / 8;                                // warp per block
         launch_plain_pdl(desc::block_reduce_kernel<In, In, 32>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
-    } else {
+    } else if (nb >= 2 * (int64_t)sms) {
         launch_plain_pdl(desc::block_reduce_cta_kernel<In, In>, (int)(nb < cap ? nb : cap), 256, 0, stream, pi, po, n, B, nb, vec);
+    } else if (nb * 8 >= 2 * (int64_t)sms) {
+        // fewer blocks than 2 per SM: an 8-CTA cluster per block (one CTA per block left
+        // 2^20-element blocks at 0.2 of peak: 64 CTAs on 148 SMs)
+        launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, 256, 0, stream, pi, po, n, B, nb, vec);
+    } else {
+        // very few blocks: 16-CTA clusters (non-portable size)
+        static const bool np = cudaFuncSetAttribute(desc::block_reduce_cluster_kernel<In, In, 16>,
+                                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+        if (np) launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 16>, (int)(nb * 16), 16, 256, 0, stream, pi, po, n, B, nb, vec);
+        else launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, 256, 0, stream, pi, po, n, B, nb, vec);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "block_reduce launch");

@@ -25,6 +25,8 @@
 #include <cstring>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "mutants.cuh"
 #include "ptx.cuh"
 
@@ -76,6 +78,11 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void *p) {
     return r;
 }
 
+// 16-byte loads in flight per lane in the reduction's body loop
+#ifndef DESC_REDUCE_UNROLL
+#define DESC_REDUCE_UNROLL 8
+#endif
+
 template <typename Acc>
 __device__ __forceinline__ Acc warp_sum(Acc v) {
 #pragma unroll
@@ -99,11 +106,21 @@ __device__ __forceinline__ Acc range_sum(const In *__restrict__ in, int64_t lo, 
     for (int64_t i = lo + lane; i < a; i += nl) acc += to_acc<Acc>(in[i]);
     const uint4 *vp = reinterpret_cast<const uint4 *>(in + a);
     int64_t k = lane;
-    for (; k + 3 * nl < nv; k += 4 * nl) {
-        const uint4 v0 = ld_nc_v4(vp + k), v1 = ld_nc_v4(vp + k + nl),
-                    v2 = ld_nc_v4(vp + k + 2 * nl), v3 = ld_nc_v4(vp + k + 3 * nl);
-        acc += vec_sum<In, Acc>(v0) + vec_sum<In, Acc>(v1) + vec_sum<In, Acc>(v2) +
-               vec_sum<In, Acc>(v3);
+    for (; k + (DESC_REDUCE_UNROLL - 1) * nl < nv; k += DESC_REDUCE_UNROLL * nl) {
+        uint4 v[DESC_REDUCE_UNROLL];
+#pragma unroll
+        for (int u = 0; u < DESC_REDUCE_UNROLL; ++u) v[u] = ld_nc_v4(vp + k + u * nl);
+#pragma unroll
+        for (int u = 0; u < DESC_REDUCE_UNROLL; ++u) acc += vec_sum<In, Acc>(v[u]);
+    }
+    if constexpr (DESC_REDUCE_UNROLL > 4) {   // short blocks: 4 loads in flight per lane
+        for (; k + 3 * nl < nv; k += 4 * nl) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = ld_nc_v4(vp + k + u * nl);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc += vec_sum<In, Acc>(v[u]);
+        }
     }
     for (; k < nv; k += nl) acc += vec_sum<In, Acc>(ld_nc_v4(vp + k));
     if (DESC_MUTANT(MUT_REDUCE_NO_TAIL)) return acc;
@@ -130,6 +147,55 @@ block_reduce_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
     }
 }
 
+// Short blocks of whole 512-byte warp rows (B * sizeof(In) = 512 P, P = 1, 2 or 4, base 16-byte
+// aligned): one warp per K = 8 / P consecutive blocks, all 8 loads of a lane in flight at
+// once, then the K warp sums interleaved (independent shuffle chains).
+template <typename In, typename Out, int P>
+__global__ void __launch_bounds__(256)
+block_reduce_rows_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t nblocks) {
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
+    using Acc = typename AccOf<In>::T;
+    constexpr int K = 8 / P;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const uint4 *vp = reinterpret_cast<const uint4 *>(in);
+    const int64_t full = nblocks / K * K;   // the rest go through the per-block loop below
+    for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32 * K; b0 < full;
+         b0 += warps * K) {
+        uint4 v[K][P];
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int p = 0; p < P; ++p) v[k][p] = ld_nc_v4(vp + ((b0 + k) * P + p) * 32 + lane);
+        Acc s[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            s[k] = 0;
+#pragma unroll
+            for (int p = 0; p < P; ++p) s[k] += vec_sum<In, Acc>(v[k][p]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < K; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+        if (lane < K) {
+            Acc t = s[0];
+#pragma unroll
+            for (int k = 1; k < K; ++k) if (lane == k) t = s[k];
+            out[b0 + lane] = (Out)t;
+        }
+    }
+    for (int64_t b = full + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; b < nblocks;
+         b += warps) {
+        Acc t = 0;
+#pragma unroll
+        for (int p = 0; p < P; ++p) t += vec_sum<In, Acc>(ld_nc_v4(vp + (b * P + p) * 32 + lane));
+        t = warp_sum(t);
+        if (lane == 0) out[b] = (Out)t;
+    }
+}
+
 // one 256-thread CTA per output block (large B)
 template <typename In, typename Out>
 __global__ void __launch_bounds__(256)
@@ -150,6 +216,48 @@ block_reduce_cta_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_
             if (threadIdx.x == 0) out[b] = (Out)t;
         }
         __syncthreads();
+    }
+}
+
+// Few, long output blocks (fewer than one 256-thread CTA per SM slot): a cluster of CL CTAs
+// per output block, each summing a contiguous 1/CL slice; rank 0 adds the CL CTA sums in
+// rank order through distributed shared memory (deterministic, no workspace, no atomics).
+template <typename In, typename Out, int CL>
+__global__ void __launch_bounds__(256)
+block_reduce_cluster_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
+                            int64_t B, int64_t nblocks, bool vec) {
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    using Acc = typename AccOf<In>::T;
+    constexpr int64_t V = 16 / sizeof(In);
+    __shared__ Acc part[8];
+    __shared__ Acc cta_sum;
+    const int r = (int)cl.block_rank();
+    const int64_t nclusters = gridDim.x / CL;
+    for (int64_t b = blockIdx.x / CL; b < nblocks; b += nclusters) {
+        const int64_t lo = b * B, hi = lo + B < n ? lo + B : n;
+        const int64_t chunk = ((hi - lo + CL - 1) / CL + V - 1) / V * V;   // slices of whole vectors
+        int64_t slo = lo + r * chunk, shi = slo + chunk;
+        if (slo > hi) slo = hi;
+        if (shi > hi) shi = hi;
+        Acc s = warp_sum(range_sum<In, Acc>(in, slo, shi, threadIdx.x, blockDim.x, vec));
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            Acc t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : Acc(0);
+            t = warp_sum(t);
+            if (threadIdx.x == 0) cta_sum = t;
+        }
+        cl.sync();                     // every CTA sum visible cluster-wide
+        if (r == 0 && threadIdx.x == 0) {
+            Acc t = 0;
+#pragma unroll
+            for (int q = 0; q < CL; ++q) t += *cl.map_shared_rank(&cta_sum, q);
+            out[b] = (Out)t;
+        }
+        cl.sync();                     // rank 0 has read every cta_sum before the next block
     }
 }
 

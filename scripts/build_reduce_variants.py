@@ -1,0 +1,15 @@
+"""Compile-time variants of the block reduction for A/B runs (DESC_LIB=<path>)."""
+import os, sys
+from concurrent.futures import ThreadPoolExecutor
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2305_03448_b200 import build as B
+
+VARIANTS = {
+    "ru4c16": ["DESC_REDUCE_UNROLL=4", "DESC_REDUCE_CTAS_PER_SM=16"],   # the earlier default
+    "norows": ["DESC_REDUCE_ROWS=0"],
+}
+out_dir = os.path.join(B.ROOT, "build_variants")
+os.makedirs(out_dir, exist_ok=True)
+with ThreadPoolExecutor(len(VARIANTS)) as ex:
+    for name, p in zip(VARIANTS, ex.map(lambda kv: B.build(defines=kv[1], out=os.path.join(out_dir, f"lib_{kv[0]}.so")), VARIANTS.items())):
+        print(name, p)

@@ -41,7 +41,14 @@ def _ulp(dt, ref):
 @pytest.mark.parametrize("n,B", [(1, 1), (1000, 1), (1000, 3), (12345, 16), (12345, 64),
                                  (100000, 65), (100000, 1000), (1 << 20, 1024),
                                  (300000, 16384), (300000, 16385), (1000003, 100000),
-                                 (50, 1000)])
+                                 (50, 1000),
+                                 # whole 512-byte warp rows per block (1, 2, 4 rows; K-block
+                                 # groups plus a remainder of blocks)
+                                 (128 * 1000 + 128 * 7, 128), (256 * 5003, 256), (512 * 77, 512),
+                                 # fewer blocks than CTA slots: cluster per block (ragged,
+                                 # near-empty last block; more blocks than clusters)
+                                 ((1 << 22) + 17, 1 << 20), (2000000, 20000),
+                                 ((1 << 24) + 5, 20000), ((1 << 24) + 3, 1 << 22)])
 def test_block_reduce(dt, n, B):
     for offset in (0, 1):
         a = _input(n, dt, n + B + offset)
