@@ -90,6 +90,16 @@ def main():
                 ok = y.cpu().numpy().tobytes() == ref.tobytes()
             bad += not ok
             print(f"block_reduce {dt.__name__} n={n} B={B}: {'ok' if ok else 'MISMATCH'}", flush=True)
+        if dt == np.float32:
+            # warp-row kernel (whole 512-byte rows per block, 1 and 2 rows) and the 8-CTA
+            # cluster kernel (40 blocks of 16400 elements)
+            for nn, B in ((512 * 128 * 3, 128), (512 * 256 + 256, 256), (40 * 16400 + 5, 16400)):
+                aa = synth.random_floats(nn, dt, 6)
+                y = desc.block_reduce(torch.from_numpy(aa).cuda(), B)
+                torch.cuda.synchronize()
+                ok = np.allclose(y.cpu().numpy(), oracle.block_reduce(aa, B), rtol=1e-6, atol=1e-6)
+                bad += not ok
+                print(f"block_reduce float32 n={nn} B={B}: {'ok' if ok else 'MISMATCH'}", flush=True)
         ref = oracle.scan(a)
         for algo in ("lookback", "three_pass", "stream"):
             y = desc.scan(x, out=torch.zeros_like(x), algo=algo)
