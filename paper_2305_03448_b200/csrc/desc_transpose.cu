@@ -1206,10 +1206,26 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
 #ifndef DESC_REDUCE_ROWS
 #define DESC_REDUCE_ROWS 1
 #endif
+#ifndef DESC_REDUCE_SEG
+#define DESC_REDUCE_SEG 1
+#endif
     const int64_t cap = (int64_t)sms * DESC_REDUCE_CTAS_PER_SM;
-    if (B <= 64) {
-        const int64_t g = (nb + 255) / 256;                            // thread per block
-        launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
+    const int64_t Bb = B * (int64_t)sizeof(In);                    // block bytes
+    if (vec && n % B == 0 && Bb % 16 == 0 && Bb <= 256 && DESC_REDUCE_SEG) {
+        // 1 … 16 vectors per block: warp-wide coalesced rows, segmented shuffles
+        const int64_t g = (nb * (Bb / 16) / 256 + 7) / 8 + 1;
+        const int grid = (int)(g < 2 * cap ? g : 2 * cap);
+        switch (Bb / 16) {
+            case 1: launch_plain_pdl(desc::block_reduce_seg_kernel<In, In, 1>, grid, 256, 0, stream, pi, po, nb); break;
+            case 2: launch_plain_pdl(desc::block_reduce_seg_kernel<In, In, 2>, grid, 256, 0, stream, pi, po, nb); break;
+            case 4: launch_plain_pdl(desc::block_reduce_seg_kernel<In, In, 4>, grid, 256, 0, stream, pi, po, nb); break;
+            case 8: launch_plain_pdl(desc::block_reduce_seg_kernel<In, In, 8>, grid, 256, 0, stream, pi, po, nb); break;
+            case 16: launch_plain_pdl(desc::block_reduce_seg_kernel<In, In, 16>, grid, 256, 0, stream, pi, po, nb); break;
+            default: {   // 3, 5, 6, 7, 9 … 15 vectors: one thread per block
+                const int64_t g1 = (nb + 255) / 256;
+                launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g1 < cap ? g1 : cap), 256, 0, stream, pi, po, n, B, nb, vec);
+            }
+        }
     } else if (vec && n % B == 0 && (B * (int64_t)sizeof(In)) % 512 == 0 &&
                B * (int64_t)sizeof(In) <= 2048 && DESC_REDUCE_ROWS) {
         // whole blocks of 1, 2 or 4 warp rows (the ragged-tail-free case; others below)
@@ -1218,6 +1234,9 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
         if (P == 1) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 1>, grid, 256, 0, stream, pi, po, nb);
         else if (P == 2) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 2>, grid, 256, 0, stream, pi, po, nb);
         else launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 4>, grid, 256, 0, stream, pi, po, nb);
+    } else if (B <= 64) {
+        const int64_t g = (nb + 255) / 256;                            // thread per block
+        launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
     } else if (B <= 16384) {
         const int64_t g = (nb + 7) / 8;                                // warp per block
         launch_plain_pdl(desc::block_reduce_kernel<In, In, 32>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);

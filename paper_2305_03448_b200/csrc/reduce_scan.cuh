@@ -196,6 +196,48 @@ block_reduce_rows_kernel(const In *__restrict__ in, Out *__restrict__ out, int64
     }
 }
 
+// Tiny blocks of VB = 1 … 16 16-byte vectors (B * sizeof(In) = 16 VB, no ragged block, base
+// 16-byte aligned): a warp reads 8 contiguous 512-byte rows at once (coalesced, unlike one
+// thread per block, whose lanes sit B elements apart), each lane sums its vector, and
+// xor-shuffles inside aligned groups of VB lanes finish each block (8 independent chains).
+template <typename In, typename Out, int VB>
+__global__ void __launch_bounds__(256)
+block_reduce_seg_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t nblocks) {
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
+    using Acc = typename AccOf<In>::T;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint4 *vp = reinterpret_cast<const uint4 *>(in);
+    const int64_t nv = nblocks * VB, full = nv / 256 * 256;
+    for (int64_t c = w * 256; c < full; c += warps * 256) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_nc_v4(vp + c + u * 32 + lane);
+        Acc s[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] = vec_sum<In, Acc>(v[u]);
+#pragma unroll
+        for (int o = VB / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+        if ((lane & (VB - 1)) == 0) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) out[(c + u * 32 + lane) / VB] = (Out)s[u];
+        }
+    }
+    // the last < 256 vectors, one 512-byte row per warp (VB divides 32: a block is wholly
+    // inside or wholly outside the array)
+    for (int64_t c = full + w * 32; c < nv; c += warps * 32) {
+        const bool live = c + lane < nv;
+        Acc s = live ? vec_sum<In, Acc>(ld_nc_v4(vp + c + lane)) : Acc(0);
+#pragma unroll
+        for (int o = VB / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (live && (lane & (VB - 1)) == 0) out[(c + lane) / VB] = (Out)s;
+    }
+}
+
 // one 256-thread CTA per output block (large B)
 template <typename In, typename Out>
 __global__ void __launch_bounds__(256)

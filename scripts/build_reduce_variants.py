@@ -5,8 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2305_03448_b200 import build as B
 
 VARIANTS = {
-    "ru4c16": ["DESC_REDUCE_UNROLL=4", "DESC_REDUCE_CTAS_PER_SM=16"],   # the earlier default
-    "norows": ["DESC_REDUCE_ROWS=0"],
+    "noseg": ["DESC_REDUCE_SEG=0"],
 }
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)

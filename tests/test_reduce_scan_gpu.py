@@ -42,6 +42,10 @@ def _ulp(dt, ref):
                                  (100000, 65), (100000, 1000), (1 << 20, 1024),
                                  (300000, 16384), (300000, 16385), (1000003, 100000),
                                  (50, 1000),
+                                 # 1 … 16 vectors per block (segmented warp rows; a
+                                 # partial last row; 3 vectors per block falls back)
+                                 (64 * 5000, 64), (16 * 777, 16), (8 * 1001, 8), (4 * 999, 4),
+                                 (32 * 4099, 32), (12 * 1000, 12),
                                  # whole 512-byte warp rows per block (1, 2, 4 rows; K-block
                                  # groups plus a remainder of blocks)
                                  (128 * 1000 + 128 * 7, 128), (256 * 5003, 256), (512 * 77, 512),
