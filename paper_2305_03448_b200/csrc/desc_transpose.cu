@@ -1209,6 +1209,13 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
 #ifndef DESC_REDUCE_SEG
 #define DESC_REDUCE_SEG 1
 #endif
+#ifndef DESC_REDUCE_ROWS_LOADS        // 16-byte loads in flight per lane in the warp-row kernel
+#define DESC_REDUCE_ROWS_LOADS 8
+#endif
+#ifndef DESC_REDUCE_ROWS_MAX          // largest block (bytes) the warp-row kernel takes
+#define DESC_REDUCE_ROWS_MAX 8192     // (4 KB blocks: 0.96 -> 1.05 of peak; profiles/r01_reduce_sweep.txt)
+#endif
+static_assert(DESC_REDUCE_ROWS_MAX <= 8192, "warp-row kernel: at most 16 rows per block");
     const int64_t cap = (int64_t)sms * DESC_REDUCE_CTAS_PER_SM;
     const int64_t Bb = B * (int64_t)sizeof(In);                    // block bytes
     if (vec && n % B == 0 && Bb % 16 == 0 && Bb <= 256 && DESC_REDUCE_SEG) {
@@ -1226,14 +1233,16 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
                 launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g1 < cap ? g1 : cap), 256, 0, stream, pi, po, n, B, nb, vec);
             }
         }
-    } else if (vec && n % B == 0 && (B * (int64_t)sizeof(In)) % 512 == 0 &&
-               B * (int64_t)sizeof(In) <= 2048 && DESC_REDUCE_ROWS) {
-        // whole blocks of 1, 2 or 4 warp rows (the ragged-tail-free case; others below)
-        const int64_t P = B * (int64_t)sizeof(In) / 512, g = (nb * P / 8 + 7) / 8 + 1;
+    } else if (vec && n % B == 0 && Bb % 512 == 0 && Bb <= DESC_REDUCE_ROWS_MAX && DESC_REDUCE_ROWS) {
+        // whole blocks of 1, 2, 4, 8 or 16 warp rows (the ragged-tail-free case; others below)
+        constexpr int L = DESC_REDUCE_ROWS_LOADS;
+        const int64_t P = Bb / 512, g = (nb * P / L + 7) / 8 + 1;
         const int grid = (int)(g < 2 * cap ? g : 2 * cap);   // 16 CTAs/SM measured best here
-        if (P == 1) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 1>, grid, 256, 0, stream, pi, po, nb);
-        else if (P == 2) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 2>, grid, 256, 0, stream, pi, po, nb);
-        else launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 4>, grid, 256, 0, stream, pi, po, nb);
+        if (P == 1) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 1, L>, grid, 256, 0, stream, pi, po, nb);
+        else if (P == 2) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 2, L>, grid, 256, 0, stream, pi, po, nb);
+        else if (P == 4) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 4, L>, grid, 256, 0, stream, pi, po, nb);
+        else if (P == 8) launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 8, (L < 8 ? 8 : L)>, grid, 256, 0, stream, pi, po, nb);
+        else launch_plain_pdl(desc::block_reduce_rows_kernel<In, In, 16, (L < 16 ? 16 : L)>, grid, 256, 0, stream, pi, po, nb);
     } else if (B <= 64) {
         const int64_t g = (nb + 255) / 256;                            // thread per block
         launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);

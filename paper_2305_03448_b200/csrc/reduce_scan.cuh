@@ -147,16 +147,16 @@ block_reduce_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
     }
 }
 
-// Short blocks of whole 512-byte warp rows (B * sizeof(In) = 512 P, P = 1, 2 or 4, base 16-byte
-// aligned): one warp per K = 8 / P consecutive blocks, all 8 loads of a lane in flight at
+// Blocks of whole 512-byte warp rows (B * sizeof(In) = 512 P, P = 1 … 16, base 16-byte
+// aligned): one warp per K = L / P consecutive blocks, all L loads of a lane in flight at
 // once, then the K warp sums interleaved (independent shuffle chains).
-template <typename In, typename Out, int P>
+template <typename In, typename Out, int P, int L = 8>
 __global__ void __launch_bounds__(256)
 block_reduce_rows_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t nblocks) {
     ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
     ptx::grid_launch_dependents();
     using Acc = typename AccOf<In>::T;
-    constexpr int K = 8 / P;
+    constexpr int K = L / P;           // blocks per warp iteration, L loads in flight per lane
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const uint4 *vp = reinterpret_cast<const uint4 *>(in);
@@ -180,6 +180,7 @@ block_reduce_rows_kernel(const In *__restrict__ in, Out *__restrict__ out, int64
 #pragma unroll
             for (int k = 0; k < K; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
         if (lane < K) {
+            static_assert(K <= 32, "one lane writes each block");
             Acc t = s[0];
 #pragma unroll
             for (int k = 1; k < K; ++k) if (lane == k) t = s[k];
