@@ -891,16 +891,19 @@ def op_arm(args, wl, world, rank, local):
     value = step_bytes * world * args.steps / (ms_max / 1e3) / 1e9
     achieved = step_bytes / (ms / args.steps / 1e3) / 1e9
     peak, peak_src = load_peak()
-    parity = None
+    parity = cpu_baseline = None
     if rank == 0 and not args.no_oracle:
         import oracle
         got = y.cpu().numpy()
+        t0 = time.perf_counter()
         if op == "reduce":
             ref = oracle.block_reduce(a, wl["block"])
+            t_oracle = time.perf_counter() - t0
             absx = oracle.block_reduce(np.abs(a).astype(np.float64), wl["block"])
             m = np.minimum(wl["block"], n - np.arange(ref.size) * wl["block"])
         else:
             ref = oracle.scan(a)
+            t_oracle = time.perf_counter() - t0
             absx = oracle.scan(np.abs(a).astype(np.float64))
             m = np.arange(1, n + 1)
         if npdt != np.int32:
@@ -910,6 +913,11 @@ def op_arm(args, wl, world, rank, local):
             parity = ("within the fp summation-order bound vs oracle" if ok else "MISMATCH")
         else:
             parity = "bit-exact vs oracle" if got.tobytes() == ref.tobytes() else "MISMATCH"
+        cpu_baseline = {"value": round(step_bytes / t_oracle / 1e9, 4), "unit": "GB/s", "cores": 1,
+                        "kind": "oracle",
+                        "sample": f"the whole workload once (the parity reference call, "
+                                  f"{t_oracle:.3f} s): oracle/reduce_scan_ref.c, 1 thread, same "
+                                  f"byte formula"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -925,11 +933,12 @@ def op_arm(args, wl, world, rank, local):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "nominal_peak": NOMINAL_HBM_GBS,
                          "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": load_traffic(args.workload),
                          "peak_source": peak_src + ("; read-only stream, may exceed a copy's "
                                                     "read+write rate" if op == "reduce" else ""),
                          "algorithmic_bytes_per_launch": step_bytes},
-            "parity": parity, "gpu_launches": launches, "cpu_baseline": None, "e2e": None,
+            "parity": parity, "gpu_launches": launches, "cpu_baseline": cpu_baseline, "e2e": None,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
