@@ -1209,6 +1209,9 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
 #ifndef DESC_REDUCE_SEG
 #define DESC_REDUCE_SEG 1
 #endif
+#ifndef DESC_REDUCE_WARP_CTAS         // grid cap (CTAs per SM) of the warp-per-block kernel
+#define DESC_REDUCE_WARP_CTAS 16
+#endif
 #ifndef DESC_REDUCE_ROWS_LOADS        // 16-byte loads in flight per lane in the warp-row kernel
 #define DESC_REDUCE_ROWS_LOADS 8
 #endif
@@ -1246,9 +1249,10 @@ static_assert(DESC_REDUCE_ROWS_MAX <= 8192, "warp-row kernel: at most 16 rows pe
     } else if (B <= 64) {
         const int64_t g = (nb + 255) / 256;                            // thread per block
         launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
-    } else if (B <= 16384) {
-        const int64_t g = (nb + 7) / 8;                                // warp per block
-        launch_plain_pdl(desc::block_reduce_kernel<In, In, 32>, (int)(g < cap ? g : cap), 256, 0, stream, pi, po, n, B, nb, vec);
+    } else if (B <= 16384 && (B < 2048 || nb >= (int64_t)sms * 32)) {
+        // (long blocks but fewer than 32 per SM: a CTA or a cluster per block, below)
+        const int64_t g = (nb + 7) / 8, wcap = (int64_t)sms * DESC_REDUCE_WARP_CTAS;   // warp per block
+        launch_plain_pdl(desc::block_reduce_kernel<In, In, 32>, (int)(g < wcap ? g : wcap), 256, 0, stream, pi, po, n, B, nb, vec);
     } else if (nb >= 2 * (int64_t)sms) {
         launch_plain_pdl(desc::block_reduce_cta_kernel<In, In>, (int)(nb < cap ? nb : cap), 256, 0, stream, pi, po, n, B, nb, vec);
     } else if (nb * 8 >= 2 * (int64_t)sms) {

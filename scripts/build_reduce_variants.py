@@ -5,9 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2305_03448_b200 import build as B
 
 VARIANTS = {
-    "l16m4k": ["DESC_REDUCE_ROWS_LOADS=16", "DESC_REDUCE_ROWS_MAX=4096"],
-    "l8m4k": ["DESC_REDUCE_ROWS_LOADS=8", "DESC_REDUCE_ROWS_MAX=4096"],
-    "l16m8k": ["DESC_REDUCE_ROWS_LOADS=16", "DESC_REDUCE_ROWS_MAX=8192"],
+    "w8": ["DESC_REDUCE_WARP_CTAS=8"],
+    "w32": ["DESC_REDUCE_WARP_CTAS=32"],
 }
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)

@@ -10,7 +10,7 @@ tag = os.path.basename(os.environ.get("DESC_LIB") or "base")
 for dt, tdt in (("f32", torch.float32), ("f64", torch.float64)):
     n = (256 << 20) // (4 if dt == "f32" else 8)
     x = torch.randn(n, dtype=tdt, device="cuda")
-    for B in (4, 8, 16, 32, 64, 128, 256, 512, 1024, 4096, 65536, 1 << 20, 1 << 22):
+    for B in (4, 8, 16, 32, 64, 128, 256, 512, 1024, 3000, 4096, 8192, 16384, 65536, 1 << 20, 1 << 22):
         y = torch.empty(-(-n // B), dtype=tdt, device="cuda")
         s = torch.cuda.current_stream().cuda_stream
         f = lambda: desc.desc_block_reduce(x.data_ptr(), y.data_ptr(), n, B, dt, s)

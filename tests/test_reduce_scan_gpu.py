@@ -49,7 +49,7 @@ def _ulp(dt, ref):
                                  # whole 512-byte warp rows per block (1, 2, 4 rows; K-block
                                  # groups plus a remainder of blocks)
                                  (128 * 1000 + 128 * 7, 128), (256 * 5003, 256), (512 * 77, 512),
-                                 (2048 * 33, 2048), (1024 * 301, 1024),
+                                 (2048 * 33, 2048), (1024 * 301, 1024), (4000 * 300 + 7, 4000),
                                  # fewer blocks than CTA slots: cluster per block (ragged,
                                  # near-empty last block; more blocks than clusters)
                                  ((1 << 22) + 17, 1 << 20), (2000000, 20000),
