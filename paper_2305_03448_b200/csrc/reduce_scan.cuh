@@ -7,9 +7,11 @@
 // Integers are summed modulo 2^bits (unsigned wrap-around; bit-exact); f32 is accumulated in
 // fp64 and rounded once on output; f64 in fp64.
 //
-// Reduction: a group of G lanes per output block (G = 1, 32 or a 256-thread CTA, chosen by
-// B); each group streams its block with 16-byte read-only loads (4 in flight per lane), a
-// scalar head/tail around the 16-byte-aligned body, then shuffles (+ shared memory for CTAs).
+// Reduction: the group that sums one output block is chosen by B and the block count (host
+// dispatch in desc_transpose.cu): lane groups of a warp (tiny blocks, segmented shuffles), a
+// warp per 1-8 blocks of whole 512-byte rows, a thread / warp / 256-thread CTA per block
+// (16-byte read-only loads, 8 in flight per lane, scalar head/tail around the aligned body),
+// or an 8- / 16-CTA cluster per block (DSMEM combine) when there are few long blocks.
 //
 // Scans (three algorithms, desc_scan_ex):
 //  * LOOKBACK: one 256 x ITEMS tile per CTA, tiles claimed in order from an atomic counter
