@@ -72,6 +72,16 @@ def test_block_reduce(dt, n, B):
             assert np.all(np.abs(got.astype(np.float64) - ref) <= tol), (n, B, offset)
 
 
+@pytest.mark.parametrize("n,B", [(1 << 20, 16), (1 << 20, 1024), (1 << 20, 5000),
+                                 ((1 << 22) + 17, 1 << 20), (2000000, 20000)])
+def test_block_reduce_repeats_bitwise(n, B):
+    """The summation order is fixed per (n, B, dtype, alignment): no atomics (header claim)."""
+    x = _dev(synth.random_floats(n, np.float32, 17), 0)
+    first = desc.block_reduce(x, B).cpu().numpy().tobytes()
+    for _ in range(3):
+        assert desc.block_reduce(x, B).cpu().numpy().tobytes() == first
+
+
 def _check_scan(got, a, dt, what):
     ref = oracle.scan(a)
     if dt in INTS:
