@@ -1209,6 +1209,11 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
 #ifndef DESC_REDUCE_SEG
 #define DESC_REDUCE_SEG 1
 #endif
+// threads per CTA of the cluster-per-block kernel: the most that keep all nb x CL CTAs in
+// one wave (2048 threads per SM), so few blocks still keep enough loads in flight
+#ifndef DESC_REDUCE_CLUSTER_THREADS
+#define DESC_REDUCE_CLUSTER_THREADS (ctas <= 2 * (int64_t)sms ? 1024 : ctas <= 4 * (int64_t)sms ? 512 : 256)
+#endif
 #ifndef DESC_REDUCE_WARP_CTAS         // grid cap (CTAs per SM) of the warp-per-block kernel
 #define DESC_REDUCE_WARP_CTAS 16
 #endif
@@ -1255,16 +1260,18 @@ static_assert(DESC_REDUCE_ROWS_MAX <= 8192, "warp-row kernel: at most 16 rows pe
         launch_plain_pdl(desc::block_reduce_kernel<In, In, 32>, (int)(g < wcap ? g : wcap), 256, 0, stream, pi, po, n, B, nb, vec);
     } else if (nb >= 2 * (int64_t)sms) {
         launch_plain_pdl(desc::block_reduce_cta_kernel<In, In>, (int)(nb < cap ? nb : cap), 256, 0, stream, pi, po, n, B, nb, vec);
-    } else if (nb * 8 >= 2 * (int64_t)sms) {
+    } else if (nb * 8 >= (int64_t)sms) {
         // fewer blocks than 2 per SM: an 8-CTA cluster per block (one CTA per block left
-        // 2^20-element blocks at 0.2 of peak: 64 CTAs on 148 SMs)
-        launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, 256, 0, stream, pi, po, n, B, nb, vec);
+        // 2^20-element blocks at 0.2 of peak: 64 CTAs on 148 SMs); CTA size adaptive
+        const int64_t ctas = nb * 8;
+        launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, DESC_REDUCE_CLUSTER_THREADS, 0, stream, pi, po, n, B, nb, vec);
     } else {
         // very few blocks: 16-CTA clusters (non-portable size)
+        const int64_t ctas = nb * 16;
         static const bool np = cudaFuncSetAttribute(desc::block_reduce_cluster_kernel<In, In, 16>,
                                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
-        if (np) launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 16>, (int)(nb * 16), 16, 256, 0, stream, pi, po, n, B, nb, vec);
-        else launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, 256, 0, stream, pi, po, n, B, nb, vec);
+        if (np) launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 16>, (int)(nb * 16), 16, DESC_REDUCE_CLUSTER_THREADS, 0, stream, pi, po, n, B, nb, vec);
+        else launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, DESC_REDUCE_CLUSTER_THREADS, 0, stream, pi, po, n, B, nb, vec);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "block_reduce launch");

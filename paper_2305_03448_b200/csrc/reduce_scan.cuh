@@ -268,7 +268,7 @@ block_reduce_cta_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_
 // per output block, each summing a contiguous 1/CL slice; rank 0 adds the CL CTA sums in
 // rank order through distributed shared memory (deterministic, no workspace, no atomics).
 template <typename In, typename Out, int CL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 block_reduce_cluster_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
                             int64_t B, int64_t nblocks, bool vec) {
     ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
@@ -277,7 +277,7 @@ block_reduce_cluster_kernel(const In *__restrict__ in, Out *__restrict__ out, in
     cg::cluster_group cl = cg::this_cluster();
     using Acc = typename AccOf<In>::T;
     constexpr int64_t V = 16 / sizeof(In);
-    __shared__ Acc part[8];
+    __shared__ Acc part[32];
     __shared__ Acc cta_sum;
     const int r = (int)cl.block_rank();
     const int64_t nclusters = gridDim.x / CL;

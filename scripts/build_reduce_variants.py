@@ -5,8 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2305_03448_b200 import build as B
 
 VARIANTS = {
-    "w8": ["DESC_REDUCE_WARP_CTAS=8"],
-    "w32": ["DESC_REDUCE_WARP_CTAS=32"],
+    "ct256": ["DESC_REDUCE_CLUSTER_THREADS=256"],
+    "ct512": ["DESC_REDUCE_CLUSTER_THREADS=512"],
 }
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)
