@@ -112,7 +112,10 @@ def load_traffic(workload: str):
 
 
 class ClockSampler:
-    """Samples SM clock and throttle reasons with NVML during the timed region."""
+    """Samples the SM clock and the throttle reasons with NVML, as fast as NVML answers, with
+    host timestamps: ``region(t0, t1)`` marks the host-time window of the timed region (from
+    just before its first event is recorded to the return of the synchronize after it), and
+    the summary reports the samples taken inside it."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -121,11 +124,13 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period_s: float = 0.002):
+    def __init__(self, index: int, period_s: float = 0.0):
         self.period = period_s
-        self.samples, self.reasons = [], set()
+        self.samples = []            # (host time, sm MHz, reason bits)
         self.ok = False
         self.max_mhz = None
+        self.t0 = self.t1 = None
+        self.extended = 0
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -141,19 +146,20 @@ class ClockSampler:
         nv = self.nv
         while not self._stop.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
+                self.samples.append((time.perf_counter(), mhz, r))
             except Exception:
                 pass
-            time.sleep(self.period)
+            if self.period:
+                time.sleep(self.period)
 
     def __enter__(self):
         if self.ok:
+            self._stop = threading.Event()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            time.sleep(0.002)        # the first samples land before the region starts
         return self
 
     def __exit__(self, *exc):
@@ -161,31 +167,51 @@ class ClockSampler:
             self._stop.set()
             self.t.join()
 
+    def region(self, t0: float, t1: float):
+        self.t0, self.t1 = t0, t1
+
+    def _in_region(self):
+        if self.t0 is None:
+            return list(self.samples)
+        return [x for x in self.samples if self.t0 <= x[0] <= self.t1]
+
     def extend(self, work, torch, dev, seconds: float = 0.3, min_samples: int = 10):
-        """A short timed region can end before NVML answers often enough: then keep sampling
-        over `seconds` of untimed repeats of the same work right after it (labelled)."""
-        if not self.ok or len(self.samples) >= min_samples:
+        """A timed region too short for min_samples NVML answers: keep sampling over `seconds`
+        of untimed repeats of the same work right after it (reported separately)."""
+        if not self.ok or len(self._in_region()) >= min_samples:
             return
-        self.in_region = len(self.samples)
-        self._stop = threading.Event()
+        n0 = len(self.samples)
         self.__enter__()
         t_end = time.time() + seconds
-        while time.time() < t_end:
-            for _ in range(20):
+        while True:
+            for _ in range(20 if seconds > 0 else 1):
                 work()
             torch.cuda.synchronize(dev)
+            if time.time() >= t_end:
+                break
         self.__exit__()
+        self.extended = len(self.samples) - n0
 
     def summary(self):
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
-        out = {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-               "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-               "samples": len(self.samples)}
-        if getattr(self, "in_region", None) is not None:
-            out["samples_in_timed_region"] = self.in_region
-            out["note"] = ("timed region too short for enough NVML samples: the rest were taken "
-                           "over 0.3 s of untimed repeats of the same step right after it")
+        inr = self._in_region()
+        use = inr if inr else self.samples
+        reasons = set()
+        for _, _, r in self.samples:
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        out = {"sm_mhz": statistics.median(m for _, m, _ in use) if use else None,
+               "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+               "samples": len(self.samples), "samples_in_timed_region": len(inr),
+               "sm_mhz_from": "samples in the timed region" if inr else "all samples"}
+        if self.extended:
+            ext = [m for _, m, _ in self.samples[-self.extended:]]
+            out["extension"] = {"samples": self.extended,
+                                "sm_mhz": statistics.median(ext),
+                                "what": "timed region gave < 10 NVML samples: 0.3 s of untimed "
+                                        "repeats of the same step right after it"}
         return out
 
 
@@ -485,6 +511,7 @@ def ours_arm(args, wl, world, rank, local):
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        t0 = time.perf_counter()
         region0.record(stream)
         for k in range(args.steps):
             if flush:
@@ -495,6 +522,7 @@ def ours_arm(args, wl, world, rank, local):
                 ends[k].record(stream)
         region1.record(stream)
         torch.cuda.synchronize(dev)
+        clk.region(t0, time.perf_counter())
     clk.extend(step, torch, dev)
     if world > 1:
         dist.barrier()
@@ -510,8 +538,9 @@ def ours_arm(args, wl, world, rank, local):
     value = total_bytes / (timed_ms_max / 1e3) / 1e9
     avg_launch_ms = timed_ms / launches            # this rank's average launch duration
     achieved = step_bytes / (avg_launch_ms / 1e3) / 1e9
-    if not flush:  # untimed diagnostic pass: per-launch spread (events between launches)
-        n_diag = min(args.steps, 200)
+    if not flush:  # untimed diagnostic pass: per-launch spread (events between launches),
+        # >= 100 launches whatever K is -- the median the paper reports
+        n_diag = max(100, min(args.steps, 200))
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_diag)]
         for k in range(n_diag):
             ev[2 * k].record(stream)
@@ -545,19 +574,6 @@ def ours_arm(args, wl, world, rank, local):
         e2e = measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, wl,
                           kernel, world)
 
-    # ---- N > 1: the real exchange step as well (configs[4] at 32768^2) --------------------
-    # NCCL all-to-all path (pipelined over row chunks; the unchunked variant timed beside it
-    # for A/B), then the fused peer-to-peer path (CUDA IPC, transposed blocks stored straight
-    # into the peers' slabs).  Ranks sharing one GPU over gloo (the 1-GPU test of this code
-    # path) can only take the peer path: gloo has no CUDA all-to-all.
-    exchange = exchange_p2p = None
-    nccl = bench_backend() == "nccl"
-    if world > 1 and args.exchange_n > 0:
-        if nccl:
-            exchange = exchange_object(world, rank, dev, args.exchange_n, "nccl")
-        if os.environ.get("DESC_BENCH_EXCHANGE_P2P", "1" if nccl else "0") == "1":
-            exchange_p2p = exchange_object(world, rank, dev, args.exchange_n, "p2p")
-
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -586,8 +602,12 @@ def ours_arm(args, wl, world, rank, local):
                          "kernel": KERNEL_FN[selected],
                          "launch_ms_mean_in_region": round(avg_launch_ms, 5),
                          "launch_spread_from": ("the timed launches" if flush else
-                                                "an untimed pass with events around each launch"),
+                                                f"an untimed pass of {len(per_launch)} launches "
+                                                "with events around each launch"),
                          "launch_ms_median": round(statistics.median(per_launch), 5),
+                         "launch_ms_median_of": len(per_launch),
+                         "median_frac": round(step_bytes / (statistics.median(per_launch) / 1e3)
+                                              / 1e9 / peak, 4),
                          "launch_ms_p10": round(float(np.percentile(per_launch, 10)), 5),
                          "launch_ms_p90": round(float(np.percentile(per_launch, 90)), 5),
                          "launch_ms_min": round(min(per_launch), 5)},
@@ -596,8 +616,6 @@ def ours_arm(args, wl, world, rank, local):
             "parity": parity,
             "gpu_launches": launches,
             **({"small_problem": small} if small else {}),
-            **({"exchange": exchange} if exchange else {}),
-            **({"exchange_p2p": exchange_p2p} if exchange_p2p else {}),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -606,66 +624,126 @@ def ours_arm(args, wl, world, rank, local):
     return 0
 
 
-def exchange_object(world, rank, dev, n, impl, steps=20, warmup=3):
-    """The `exchange` / `exchange_p2p` object of the N > 1 replica line: one n x n f32 slab
-    transpose over all ranks (strong scaling).  A Python-level failure is reported in the
-    object and leaves the replica line intact."""
-    try:
-        r = slab_exchange(world, rank, dev, n, impl, steps, warmup)
-        obj = {"workload": f"{n}x{n} f32 distributed transpose, row slabs + {impl} exchange "
-                           "(configs[4] shape, smaller matrix)",
-               "value": round(r["value"], 2), "unit": "GB/s",
-               "ms_per_step": round(r["ms_max"] / steps, 4), "scaling": "strong",
-               "roofline": r["roofline"], "parity": r["parity"], "gpu_launches": r["launches"]}
-        if impl == "nccl":
-            obj["chunks"] = r["chunks"]
-            if r["chunks"] > 1:   # A/B: the same exchange without the pipeline
-                r1 = slab_exchange(world, rank, dev, n, impl, steps, warmup, chunks=1)
-                obj["unchunked"] = {"ms_per_step": round(r1["ms_max"] / steps, 4),
-                                    "frac": r1["roofline"]["frac"], "parity": r1["parity"]}
-        return obj
-    except Exception as e:  # noqa: BLE001
-        return {"error": f"{type(e).__name__}: {e}"[:300]}
+# ------------------------------------------------------------------------- configs[4]
+class _Done:
+    def wait(self):
+        return True
 
 
-def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4, chunks=None):
-    """One distributed transpose of an n x n f32 matrix held as row slabs (configs[4]; NCCL
-    all-to-all path, or the fused IPC peer path): returns the measured figures.  The input is
-    the counter hash generated in HBM; parity is checked on sampled 64 x 64 blocks of every
-    rank's output slab against the oracle."""
+def staged_all_to_all(out, inp, group=None, async_op=False):
+    """DESC_BENCH_BACKEND=gloo only (several ranks sharing ONE GPU to exercise the N > 1 code
+    path on a 1-GPU box): the all-to-all through host memory -- gloo has no CUDA all-to-all
+    and NCCL refuses two ranks on one GPU.  Never used with the NCCL backend."""
     import torch
     import torch.distributed as dist
-    import oracle
+    torch.cuda.synchronize()
+    o = torch.empty(out.shape, dtype=out.dtype)
+    dist.all_to_all_single(o, inp.cpu(), group=group)
+    out.copy_(o)
+    return _Done()
+
+
+def slab_roofline(lay, es, step_s):
+    """T* = max(2S / HBM, S(P-1)/P / NVLink) per rank; frac = T* / t_step."""
+    peak, peak_src = load_peak()
+    S = lay.Rm * lay.N * es
+    t_hbm = 2 * S / (peak * 1e9)
+    t_nvl = lay.nvlink_bytes(es) / (NVLINK_PEER_GBS * 1e9)
+    t_star = max(t_hbm, t_nvl)
+    hbm_bound = t_hbm >= t_nvl
+    return {"bound": "hbm" if hbm_bound else "nvlink",
+            "achieved": round((2 * S if hbm_bound else lay.nvlink_bytes(es)) / step_s / 1e9, 2),
+            "peak": peak if hbm_bound else NVLINK_PEER_GBS,
+            "unit": "GB/s", "frac": round(t_star / step_s, 4), "traffic": None,
+            "t_star_ms": round(t_star * 1e3, 4), "t_hbm_ms": round(t_hbm * 1e3, 4),
+            "t_nvlink_ms": round(t_nvl * 1e3, 4),
+            "peak_source": peak_src + "; NVLink: B200_PROFILING.md measured peer copy 770 GB/s "
+                                      "per direction",
+            "note": "frac = T*/t_step, T* = max(2S/HBM, S(P-1)/P / 770 GB/s), S = slab bytes"}
+
+
+def slab_buffers(world, rank, dev, n, es=4, ws=True):
+    """Rank's input slab (hash-filled in HBM: in[i][j] = H(seed, i*n + j)), its output slab and
+    the NCCL path's (send, recv) workspace."""
+    import torch
     from paper_2305_03448_b200 import dist as ddist
+    lay = ddist.SlabLayout(n, n, world, rank)
+    it = {4: torch.int32, 8: torch.int64}[es]
+    x = torch.empty((lay.Rm, lay.N), dtype=it, device=dev)
+    synth.hash_fill_torch(x, lay.in_rows()[0], 0, lay.N, SLAB_SEED, chunk_rows=1024)
+    out = torch.empty((lay.Rn, lay.M), dtype=it, device=dev)
+    w = None
+    if ws:
+        w = (torch.empty(lay.Rm * lay.N, dtype=it, device=dev),
+             torch.empty(lay.Rm * lay.N, dtype=it, device=dev))
+    return lay, x, out, w
 
-    M = N = n
-    lay = ddist.SlabLayout(M, N, world, rank)
-    seed = synth.BASE_SEED + 5
-    x = torch.empty((lay.Rm, N), dtype=torch.int32, device=dev)
-    synth.hash_fill_torch(x, lay.in_rows()[0], 0, N, seed, chunk_rows=1024)
-    x = x.view(torch.float32)
-    out = torch.empty((lay.Rn, M), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    impl = impl if world > 1 else "local"
-    C = None
+
+SLAB_SEED = synth.BASE_SEED + 5
+
+
+def slab_verify(lay, out, dev, blocks: int = 4):
+    """EVERY element of this rank's output slab against the closed form of the hash input
+    (tests/fullcheck.py), plus `blocks` 64 x 64 blocks against the oracle itself; the verdict
+    is the min over ranks."""
+    import torch
+    import oracle
+    from tests.fullcheck import hash_transpose_mismatches
+    r0, _ = lay.out_rows()
+    bad, first = hash_transpose_mismatches(out, r0, lay.N, SLAB_SEED, chunk_rows=512)
+    rng = np.random.default_rng(SLAB_SEED + lay.r)
+    es = out.element_size()
+    picks = [(0, 0), (lay.Rn - 64, lay.M - 64)] + [
+        (int(rng.integers(0, lay.Rn - 63)), int(rng.integers(0, lay.M - 63)))
+        for _ in range(blocks)]
+    ok_blocks = True
+    for j0, i0 in picks:           # out_r[j0:j0+64, i0:i0+64] = A[i0:i0+64, r0+j0:r0+j0+64]^T
+        j0, i0 = max(0, j0), max(0, i0)
+        h = min(64, lay.Rn - j0)
+        w = min(64, lay.M - i0)
+        ii, jj = np.meshgrid(np.arange(i0, i0 + w), np.arange(r0 + j0, r0 + j0 + h), indexing="ij")
+        exp = oracle.transpose(synth.hash_expected_np(ii, jj, lay.N, SLAB_SEED, es))
+        got = out[j0:j0 + h, i0:i0 + w].cpu().numpy().view(exp.dtype)
+        ok_blocks &= got.tobytes() == exp.tobytes()
+    total_bad = reduce_scalar(float(bad), "max", dev)
+    all_ok = reduce_scalar(1.0 if (bad == 0 and ok_blocks) else 0.0, "min", dev) > 0.5
+    if all_ok:
+        return (f"bit-exact: every element of every rank's slab ({lay.M * lay.N} in total) vs the "
+                "closed form of the hash input, plus 64x64 blocks vs the oracle")
+    return f"MISMATCH (max over ranks {int(total_bad)} elements; rank {lay.r} first at {first})"
+
+
+def slab_step_fn(impl, lay, x, out, ws, chunks, group=None):
+    """One distributed transpose step; returns (step(), chunks) -- step() returns the number of
+    our kernel launches it made."""
+    from paper_2305_03448_b200 import dist as ddist
     if impl == "p2p":
-        xp = ddist.PeerSlabTranspose(out, M)
-        # steps back to back without the per-call group barriers: inside this loop no rank
-        # reads its slab, and ranks write disjoint column blocks of each slab in stream
-        # order, so the only barrier the result needs is the one after the last step (the
-        # region is timed by CUDA events on each rank's stream, max over ranks)
-        step = lambda: xp(x, barrier=False)[1]                       # noqa: E731
-    else:
-        ws = None
-        if world > 1:
-            ws = (torch.empty(lay.Rm * N, dtype=torch.float32, device=dev),
-                  torch.empty(lay.Rm * N, dtype=torch.float32, device=dev))
+        xp = ddist.PeerSlabTranspose(out, lay.M, group=group,
+                                     force_remote=bench_backend() != "nccl")
+        # back to back without the per-call group barriers: inside the loop no rank reads its
+        # slab and the ranks write disjoint column blocks of each slab in stream order, so
+        # the result only needs the barrier after the last step (taken by the caller)
+        return (lambda: xp(x, barrier=False)[1]), None, xp
+    if impl == "local":
+        def step_local():
+            ddist.slab_transpose(x, out)
+            return 1
+        return step_local, 1, None
+    a2a = staged_all_to_all if bench_backend() != "nccl" else None
+    C = ddist.default_chunks(lay.Rm, lay.P) if chunks is None else chunks
 
-        C = ddist.default_chunks(lay.Rm, world) if chunks is None else chunks
+    def step():
+        ddist.slab_transpose(x, out, workspace=ws, chunks=C, all_to_all=a2a, group=group)
+        return 2 * C
+    return step, C, None
 
-        def step():
-            ddist.slab_transpose(x, out, workspace=ws, chunks=C)
-            return 2 * C if world > 1 else 1                         # our kernels per step
+
+def timed_region(step, steps, warmup, dev, world):
+    """W untimed steps, then EXACTLY K steps between a barrier + synchronize on both sides,
+    CUDA events on the launch stream, NVML clocks sampled in the region; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream(dev)
     for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -675,53 +753,127 @@ def slab_exchange(world, rank, dev, n, impl, steps, warmup, es=4, chunks=None):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(steps):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1)
-    ms_max = reduce_scalar(ms, "max", dev)
-    step_s = ms_max / steps / 1e3
-    value = 2 * M * N * es * steps / (ms_max / 1e3) / 1e9
-    peak, peak_src = load_peak()
-    S = lay.Rm * N * es
-    t_hbm = 2 * S / (peak * 1e9)
-    t_nvl = lay.nvlink_bytes(es) / (NVLINK_PEER_GBS * 1e9)
-    t_star = max(t_hbm, t_nvl)
-    rng = np.random.default_rng(seed + rank)
-    r0, _ = lay.out_rows()
-    picks = [(0, 0), (lay.Rn - 64, M - 64)] + [
-        (int(rng.integers(0, lay.Rn - 64)), int(rng.integers(0, M - 64))) for _ in range(6)]
-    ok = True
-    for j0, i0 in picks:           # out_r[j0:j0+64, i0:i0+64] = A[i0:i0+64, r0+j0:r0+j0+64]^T
-        ii, jj = np.meshgrid(np.arange(i0, i0 + 64), np.arange(r0 + j0, r0 + j0 + 64), indexing="ij")
-        exp = oracle.transpose(synth.hash_expected_np(ii, jj, N, seed, es))
-        got = out[j0:j0 + 64, i0:i0 + 64].view(torch.int32).cpu().numpy().view(np.uint32)
-        ok &= got.tobytes() == exp.tobytes()
-    all_ok = reduce_scalar(1.0 if ok else 0.0, "min", dev) > 0.5
-    if impl == "p2p":
-        xp.close()
-    del x, out
-    return {
-        "value": value, "ms_max": ms_max, "impl": impl, "launches": launches, "lay": lay,
-        "chunks": C,
-        "clocks": clk.summary(),
-        "roofline": {"bound": "hbm" if t_hbm >= t_nvl else "nvlink",
-                     "achieved": round((2 * S if t_hbm >= t_nvl else lay.nvlink_bytes(es))
-                                       / step_s / 1e9, 2),
-                     "peak": peak if t_hbm >= t_nvl else NVLINK_PEER_GBS,
-                     "unit": "GB/s", "frac": round(t_star / step_s, 4), "traffic": None,
-                     "t_star_ms": round(t_star * 1e3, 4), "t_hbm_ms": round(t_hbm * 1e3, 4),
-                     "t_nvlink_ms": round(t_nvl * 1e3, 4), "peak_source": peak_src,
-                     "note": "frac = T*/t_step, T* = max(2S/HBM, S(P-1)/P / 770 GB/s)"},
-        "parity": "sampled 64x64 blocks bit-exact vs oracle" if all_ok else "MISMATCH",
-    }
+        clk.region(t0, time.perf_counter())
+    if world > 1:
+        dist.barrier()
+    ms_max = reduce_scalar(e0.elapsed_time(e1), "max", dev)
+    # too few NVML samples in the region: every rank repeats the step the SAME number of
+    # times (the steps may contain collectives), decided from values equal on all ranks
+    short = reduce_scalar(1.0 if clk.ok and len(clk._in_region()) < 10 else 0.0, "max", dev)
+    if short > 0.5:
+        reps = max(1, min(2000, int(0.3 / max(ms_max / steps / 1e3, 1e-6))))
+        clk.extend(lambda: [step() for _ in range(reps)], torch, dev, seconds=0.0, min_samples=10**9)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    return ms_max, launches, clk
+
+
+def slab_phases(lay, x, out, ws, dev, world, reps: int = 3):
+    """The NCCL path's three phases timed separately (unchunked: pack = local transpose into
+    the send buffer, the all-to-all, unpack), median of `reps`, each the max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2305_03448_b200 as desc
+    stream = torch.cuda.current_stream(dev)
+    send, recv = (w.view(-1) for w in ws)
+    a2a = dist.all_to_all_single if bench_backend() == "nccl" else staged_all_to_all
+    N, Rm, Rn, M, P = lay.N, lay.Rm, lay.Rn, lay.M, lay.P
+    ts = []
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ev[0].record(stream)
+        desc.transpose(x, send[:N * Rm].view(N, Rm))
+        ev[1].record(stream)
+        a2a(recv[:N * Rm], send[:N * Rm])
+        ev[2].record(stream)
+        desc.desc_copy_batched(recv.data_ptr(), out.data_ptr(), P, Rn, Rm, Rm, M, Rn * Rm, Rm,
+                               out.dtype, stream.cuda_stream)
+        ev[3].record(stream)
+        torch.cuda.synchronize(dev)
+        ts.append([ev[k].elapsed_time(ev[k + 1]) for k in range(3)])
+    med = [statistics.median(t[k] for t in ts) for k in range(3)]
+    med = [reduce_scalar(v, "max", dev) for v in med]
+    S = Rm * N * out.element_size()
+    peak, _ = load_peak()
+    return {"pack_ms": round(med[0], 4), "all_to_all_ms": round(med[1], 4),
+            "unpack_ms": round(med[2], 4), "sum_ms": round(sum(med), 4),
+            "pack_hbm_frac": round(2 * S / (med[0] / 1e3) / 1e9 / peak, 4),
+            "unpack_hbm_frac": round(2 * S / (med[2] / 1e3) / 1e9 / peak, 4),
+            "all_to_all_gbs_per_direction": round(lay.nvlink_bytes(out.element_size())
+                                                  / (med[1] / 1e3) / 1e9, 2),
+            "what": "unchunked step, phases timed by CUDA events on the compute stream (the "
+                    "all-to-all synchronous), median of 3, max over ranks"
+                    + ("" if bench_backend() == "nccl" else
+                       "; all-to-all staged through the host (gloo 1-GPU test mode)")}
+
+
+def replicas_object(world, rank, dev, steps: int = 50, warmup: int = 5):
+    """Weak-scaling context at N > 1: one 8192^2 f32 transpose per rank (configs[2] replicas,
+    no collective), K launches back to back, max over ranks."""
+    import torch
+    import paper_2305_03448_b200 as desc
+    x = torch.from_numpy(synth.random_bits((8192, 8192), 4, synth.BASE_SEED + 2 + 1000 * rank)
+                         .view(np.int32)).to(dev)
+    y = torch.empty_like(x)
+    ms, launches, clk = timed_region(lambda: (desc.transpose(x, y), 1)[1], steps, warmup, dev, world)
+    peak, _ = load_peak()
+    step_bytes = 2 * 8192 * 8192 * 4
+    value = step_bytes * world * steps / (ms / 1e3) / 1e9
+    ok = bool(torch.equal(y[:64, :64], x[:64, :64].t()))
+    del x, y
+    return {"workload": "8192x8192 f32 per rank (configs[2] replicas, no collective)",
+            "value": round(value, 2), "unit": "GB/s", "scaling": "weak",
+            "ms_per_step": round(ms / steps, 5), "frac_per_gpu": round(value / world / peak, 4),
+            "gpu_launches": launches, "spot_check": "ok" if ok else "MISMATCH"}
+
+
+def dist_e2e(world, rank, dev, n, steps: int = 5):
+    """configs[4]'s e2e through the public API at a bounded size (n x n, host memory per rank
+    2 * n^2 * 4 / P bytes): every step copies this rank's input slab from pinned host memory,
+    runs the distributed transpose, and copies its output slab back to pinned host memory."""
+    import torch
+    from paper_2305_03448_b200 import dist as ddist
+    lay, x, out, ws = slab_buffers(world, rank, dev, n, ws=world > 1)
+    h_in = x.cpu().pin_memory()
+    h_out = torch.empty((lay.Rn, lay.M), dtype=x.dtype, pin_memory=True)
+    a2a = staged_all_to_all if bench_backend() != "nccl" else None
+
+    def step():
+        x.copy_(h_in, non_blocking=True)
+        ddist.slab_transpose(x, out, workspace=ws, all_to_all=a2a)
+        h_out.copy_(out, non_blocking=True)
+        return 2 * ddist.default_chunks(lay.Rm, world) if world > 1 else 1
+    ms, launches, _ = timed_region(step, steps, 3, dev, world)
+    out.copy_(h_out)                   # what reached the host, verified on the device
+    parity = slab_verify(lay, out, dev, blocks=1)
+    es = 4
+    value = 2 * n * n * es * steps / (ms / 1e3) / 1e9
+    bi = lay.Rm * lay.N * es
+    del x, out, ws
+    return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": bi * world,
+            "d2h_bytes_per_step": bi * world, "bytes_per_rank_each_way": bi,
+            "workload": f"{n}x{n} f32 (configs[4] layout at a host-memory-bounded size)",
+            "steps": steps, "gpu_launches": launches, "parity": parity,
+            "path": "pinned host slab -> H2D -> slab_transpose (public API) -> D2H -> pinned "
+                    "host slab, every step"}
 
 
 def dist_arm(args, wl, world, rank, local):
-    """configs[4]: the global M x N matrix lives as row slabs, one per rank; a step is one
-    full distributed transpose (slab_transpose over NCCL, or the fused IPC peer path)."""
+    """configs[4]: the global n x n matrix lives as row slabs, one per rank; a step is one
+    full distributed transpose.  Headline: the NCCL all-to-all path (pipelined over row
+    chunks) with strong scaling; beside it the fused peer-to-peer path
+    (exchange_p2p), the phases of the NCCL path, the 8192^2 replicas (weak), e2e; every
+    element of every rank's slab verified after each path."""
     import torch
     import torch.distributed as dist
     import paper_2305_03448_b200 as desc
@@ -732,25 +884,80 @@ def dist_arm(args, wl, world, rank, local):
     desc.load()
     if world > 1:
         init_pg(dev)
-    r = slab_exchange(world, rank, dev, args.dist_n, args.dist_impl, args.steps, args.warmup,
-                      wl["es"], chunks=args.dist_chunks)
-    lay = r["lay"]
+    n, es = args.dist_n, wl["es"]
+    impl = args.dist_impl if world > 1 else "local"
+    lay, x, out, ws = slab_buffers(world, rank, dev, n, es, ws=world > 1)
+
+    def run(impl_, chunks=None):
+        out.fill_(0x5A5A5A5A)
+        step, C, xp = slab_step_fn(impl_, lay, x, out, ws, chunks)
+        ms, launches, clk = timed_region(step, args.steps, args.warmup, dev, world)
+        if xp is not None:
+            xp.close()
+        parity = slab_verify(lay, out, dev)
+        step_s = ms / args.steps / 1e3
+        return {"ms": ms, "launches": launches, "clk": clk, "chunks": C, "parity": parity,
+                "value": 2 * lay.M * lay.N * es * args.steps / (ms / 1e3) / 1e9,
+                "roofline": slab_roofline(lay, es, step_s)}
+
+    head = run(impl, args.dist_chunks)
+    extra = {}
+    if world > 1:
+        other = "p2p" if impl == "nccl" else "nccl"
+        try:
+            r = run(other)
+            extra["exchange_p2p" if other == "p2p" else "exchange_nccl"] = {
+                "impl": other, "value": round(r["value"], 2), "unit": "GB/s",
+                "ms_per_step": round(r["ms"] / args.steps, 4), "roofline": r["roofline"],
+                "parity": r["parity"], "gpu_launches": r["launches"], "chunks": r["chunks"],
+                "what": ("fused transpose + exchange: one kernel per destination writes block "
+                         "(r,s)^T straight into rank s's slab through CUDA IPC (2S HBM per rank)"
+                         if other == "p2p" else "NCCL all-to-all path")}
+        except Exception as e:  # noqa: BLE001  (reported, the headline stays)
+            extra["exchange_" + other] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        if impl == "nccl" and head["chunks"] > 1:
+            r1 = run("nccl", 1)
+            extra["unchunked"] = {"ms_per_step": round(r1["ms"] / args.steps, 4),
+                                  "frac": r1["roofline"]["frac"], "parity": r1["parity"]}
+        try:
+            extra["phases"] = slab_phases(lay, x, out, ws, dev, world)
+        except Exception as e:  # noqa: BLE001
+            extra["phases"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    del x, out, ws
+    torch.cuda.empty_cache()
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_oracle:
+        r = run_oracle(wl, budget_s=args.oracle_seconds)
+        cpu_baseline = {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                        "sample": r["sample"], "host": host_info()}
+    e2e = None
+    if not args.no_e2e:
+        e2e = dist_e2e(world, rank, dev, min(n, args.dist_e2e_n))
+    if world > 1:
+        extra["replicas"] = replicas_object(world, rank, dev)
     if rank == 0:
+        rf = dict(head["roofline"])
         line = {
-            "metric": METRIC, "value": round(r["value"], 2), "unit": "GB/s", "n_gpus": world,
+            "metric": METRIC, "value": round(head["value"], 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(r["ms_max"] / args.steps, 4), "higher_is_better": True,
+            "ms_per_step": round(head["ms"] / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"],
             "data": "synthetic (counter-based hash, generated in HBM)",
             "config": {"workload": wl["name"], "rows": lay.M, "cols": lay.N, "ranks": world,
-                       "slab_rows": lay.Rm, "impl": r["impl"], "chunks": r["chunks"],
-                       "parallelism": f"row slabs over {world} rank(s)",
-                       "l2": "inputs larger than L2, no flush",
-                       "timing": "CUDA events around K steps, max over ranks"},
-            "roofline": r["roofline"],
-            "parity": r["parity"],
-            "gpu_launches": r["launches"], "cpu_baseline": None, "e2e": None,
-            "clocks": r["clocks"],
+                       "slab_rows": lay.Rm, "impl": impl, "chunks": head["chunks"],
+                       "parallelism": (f"row slabs over {world} ranks, "
+                                       + ("NCCL all-to-all" if impl == "nccl" else
+                                          "fused peer-to-peer stores") if world > 1 else
+                                       "one rank: a single local transpose"),
+                       "backend": bench_backend() if world > 1 else None,
+                       "l2": "inputs larger than L2 (slab >= 2 GiB), no flush",
+                       "timing": "CUDA events around exactly K steps after barrier + "
+                                 "synchronize, max over ranks"},
+            "roofline": rf,
+            "parity": head["parity"],
+            "gpu_launches": head["launches"], "cpu_baseline": cpu_baseline, "e2e": e2e,
+            **extra,
+            "clocks": head["clk"].summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -790,11 +997,14 @@ def view_arm(args, wl, world, rank, local):
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
+        clk.region(t0, time.perf_counter())
+    clk.extend(step, torch, dev)
     ms = e0.elapsed_time(e1)
     ms_max = reduce_scalar(ms, "max", dev)
     step_bytes = 2 * rows * cols * es
@@ -881,11 +1091,14 @@ def op_arm(args, wl, world, rank, local):
     launches = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
+        clk.region(t0, time.perf_counter())
+    clk.extend(step, torch, dev)
     ms = e0.elapsed_time(e1)
     ms_max = reduce_scalar(ms, "max", dev)
     value = step_bytes * world * args.steps / (ms_max / 1e3) / 1e9
@@ -1026,7 +1239,9 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="8192f32")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None,
+                    help="default: 8192f32 at N = 1 (configs[2], the headline target), "
+                         "dist65536 at N > 1 (configs[4], the distributed transpose)")
     ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem", "tiled"], default="auto")
     ap.add_argument("--scan-algo", choices=["auto", "lookback", "three_pass", "stream"],
                     default="auto")
@@ -1041,9 +1256,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--l2", choices=["rotate", "flush"], default="rotate",
                     help="how a working set smaller than 2 x L2 is kept out of L2")
-    ap.add_argument("--exchange-n", type=int, default=32768,
-                    help="N > 1 default workload: also time one n x n slab transpose with the "
-                         "NCCL all-to-all (0: skip)")
+    ap.add_argument("--dist-e2e-n", type=int, default=16384,
+                    help="matrix side of the dist workload's e2e measurement (host memory bound)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
@@ -1051,6 +1265,8 @@ def main():
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    if args.workload is None:
+        args.workload = "dist65536" if world > 1 else "8192f32"
     wl = dict(WORKLOADS[args.workload])
     if wl.get("dist") and args.impl == "ours":
         return dist_arm(args, wl, world, rank, local)

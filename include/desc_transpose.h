@@ -223,7 +223,10 @@ desc_status desc_view_copy(const void *in, void *out, const desc_strided_view *v
  * out has the input's dtype.  Integers (DESC_U8, DESC_I32, DESC_I64) sum modulo 2^bits
  * (bit-exact); DESC_F32 accumulates in fp64 and rounds once; DESC_F64 in fp64 (float results
  * depend on the summation order only within the usual gamma_B * sum|x| bound; the order is
- * fixed for a given n, block, dtype and input alignment: no atomics, runs repeat bit for bit;
+ * fixed for a given n, block, dtype, input alignment and device (its SM count and occupancy
+ * pick the summing group -- warp, CTA or cluster -- and the CTA size, so f32/f64 sums may
+ * differ in the last bits between devices or MIG slices): no atomics, runs on one device
+ * repeat bit for bit;
  * the launch configuration is derived inside).  DESC_F16 /
  * DESC_BF16 give DESC_ERR_DTYPE; block <= 0 or n < 0 give DESC_ERR_SHAPE; in/out overlap
  * gives DESC_ERR_ALIAS.  Asynchronous on `stream`. */

@@ -226,6 +226,14 @@ def desc_scan_ex(in_ptr, out_ptr, n, dtype, d_work_ptr, work_bytes, algo="auto",
                                       stream))
 
 
+def _check_out(out, x, numel: int) -> None:
+    """The C ABI takes no output size: a wrong `out` would be written out of bounds."""
+    if (not out.is_contiguous() or out.device != x.device or out.dtype != x.dtype
+            or out.numel() != numel):
+        raise ValueError(f"out must be a contiguous {x.dtype} tensor of {numel} elements "
+                         f"on {x.device}")
+
+
 def block_reduce(x, block: int, out=None):
     """Per-block sums of a contiguous 1-D CUDA tensor (see desc_block_reduce)."""
     import torch
@@ -233,6 +241,7 @@ def block_reduce(x, block: int, out=None):
     nb = -(-x.numel() // block) if block > 0 else 0
     if out is None:
         out = torch.empty(nb, dtype=x.dtype, device=x.device)
+    _check_out(out, x, nb)
     desc_block_reduce(x.data_ptr(), out.data_ptr(), x.numel(), block, x.dtype, _stream_of(x))
     return out
 
@@ -243,6 +252,7 @@ def scan(x, out=None, work=None, algo="auto"):
     x = x.reshape(-1)
     if out is None:
         out = torch.empty_like(x)
+    _check_out(out, x, x.numel())
     nbytes = desc_scan_workspace(x.numel(), x.dtype)
     if work is None:
         work = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=x.device)

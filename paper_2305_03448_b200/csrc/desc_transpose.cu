@@ -246,12 +246,19 @@ bool tma_store_ok(const Args &a) { return (a.es == 4 || a.es == 8) && a.rows * a
 // (device, stream), allocated on first use (the only device memory the library owns;
 // 16 bytes per stream, never freed) and self-reset by the last CTA of every launch.  Launches
 // on one stream are ordered, so they can share a counter; different streams get different
-// counters, so concurrent launches never share one.
+// counters, so concurrent launches never share one.  Streams are told apart by
+// cudaStreamGetId, not by the handle: the per-thread default stream has the same handle
+// (cudaStreamPerThread) in every host thread but a distinct id per thread.  Launches being
+// captured into a CUDA graph never use a counter (static schedule): a replay of the graph
+// on another stream could otherwise race a live launch on the captured stream's counter.
 std::mutex g_sched_mu;
 std::unordered_map<uint64_t, unsigned long long *> g_sched;
 
 desc_status sched_counter(int dev, cudaStream_t stream, unsigned long long **out) {
-    const uint64_t key = (uint64_t)reinterpret_cast<uintptr_t>(stream) * 64 + (uint64_t)dev;
+    unsigned long long sid = 0;
+    cudaError_t ge = cudaStreamGetId(stream, &sid);
+    if (ge != cudaSuccess) return cuda_fail(ge, "cudaStreamGetId");
+    const uint64_t key = (uint64_t)sid * 64 + (uint64_t)dev;
     std::lock_guard<std::mutex> lk(g_sched_mu);
     auto it = g_sched.find(key);
     if (it != g_sched.end()) { *out = it->second; return DESC_OK; }
@@ -263,13 +270,6 @@ desc_status sched_counter(int dev, cudaStream_t stream, unsigned long long **out
     g_sched.emplace(key, static_cast<unsigned long long *>(p));
     *out = static_cast<unsigned long long *>(p);
     return DESC_OK;
-}
-
-void sched_lookup(int dev, cudaStream_t stream, unsigned long long **out) {
-    const uint64_t key = (uint64_t)reinterpret_cast<uintptr_t>(stream) * 64 + (uint64_t)dev;
-    std::lock_guard<std::mutex> lk(g_sched_mu);
-    auto it = g_sched.find(key);
-    *out = it == g_sched.end() ? nullptr : it->second;
 }
 
 // Launch with programmatic stream serialisation (PDL) so that back-to-back transposes
@@ -448,15 +448,11 @@ desc_status launch_tma2(const Args &a) {
     if (dyn && p.ntiles >= (int64_t)dyn_min * grid) {
         int dev = 0;
         cudaGetDevice(&dev);
-        // a stream being captured into a CUDA graph cannot allocate: use an existing
-        // counter if there is one, else fall back to static scheduling
+        // under graph capture: static scheduling (see sched_counter)
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(a.stream, &cap);
-        if (cap == cudaStreamCaptureStatusNone) {
+        if (cap == cudaStreamCaptureStatusNone)
             if (desc_status s = sched_counter(dev, a.stream, &p.sched)) return s;
-        } else {
-            sched_lookup(dev, a.stream, &p.sched);
-        }
     }
     CUtensorMap min, mout;
     if (desc_status s = in_map(a, TR, &min)) return s;
@@ -1209,11 +1205,6 @@ desc_status launch_reduce(const void *in, void *out, int64_t n, int64_t B, int64
 #ifndef DESC_REDUCE_SEG
 #define DESC_REDUCE_SEG 1
 #endif
-// threads per CTA of the cluster-per-block kernel: the most that keep all nb x CL CTAs in
-// one wave (2048 threads per SM), so few blocks still keep enough loads in flight
-#ifndef DESC_REDUCE_CLUSTER_THREADS
-#define DESC_REDUCE_CLUSTER_THREADS (ctas <= 2 * (int64_t)sms ? 1024 : ctas <= 4 * (int64_t)sms ? 512 : 256)
-#endif
 #ifndef DESC_REDUCE_WARP_CTAS         // grid cap (CTAs per SM) of the warp-per-block kernel
 #define DESC_REDUCE_WARP_CTAS 16
 #endif
@@ -1241,8 +1232,10 @@ static_assert(DESC_REDUCE_ROWS_MAX <= 8192, "warp-row kernel: at most 16 rows pe
                 launch_plain_pdl(desc::block_reduce_kernel<In, In, 1>, (int)(g1 < cap ? g1 : cap), 256, 0, stream, pi, po, n, B, nb, vec);
             }
         }
-    } else if (vec && n % B == 0 && Bb % 512 == 0 && Bb <= DESC_REDUCE_ROWS_MAX && DESC_REDUCE_ROWS) {
-        // whole blocks of 1, 2, 4, 8 or 16 warp rows (the ragged-tail-free case; others below)
+    } else if (vec && n % B == 0 && Bb % 512 == 0 && Bb <= DESC_REDUCE_ROWS_MAX &&
+               ((Bb / 512) & (Bb / 512 - 1)) == 0 && DESC_REDUCE_ROWS) {
+        // whole blocks of 1, 2, 4, 8 or 16 warp rows (the ragged-tail-free case; other row
+        // counts -- 3, 5, 6, 7, 9 ... 15 -- take the warp-per-block kernel below)
         constexpr int L = DESC_REDUCE_ROWS_LOADS;
         const int64_t P = Bb / 512, g = (nb * P / L + 7) / 8 + 1;
         const int grid = (int)(g < 2 * cap ? g : 2 * cap);   // 16 CTAs/SM measured best here
@@ -1260,18 +1253,42 @@ static_assert(DESC_REDUCE_ROWS_MAX <= 8192, "warp-row kernel: at most 16 rows pe
         launch_plain_pdl(desc::block_reduce_kernel<In, In, 32>, (int)(g < wcap ? g : wcap), 256, 0, stream, pi, po, n, B, nb, vec);
     } else if (nb >= 2 * (int64_t)sms) {
         launch_plain_pdl(desc::block_reduce_cta_kernel<In, In>, (int)(nb < cap ? nb : cap), 256, 0, stream, pi, po, n, B, nb, vec);
-    } else if (nb * 8 >= (int64_t)sms) {
-        // fewer blocks than 2 per SM: an 8-CTA cluster per block (one CTA per block left
-        // 2^20-element blocks at 0.2 of peak: 64 CTAs on 148 SMs); CTA size adaptive
-        const int64_t ctas = nb * 8;
-        launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, DESC_REDUCE_CLUSTER_THREADS, 0, stream, pi, po, n, B, nb, vec);
     } else {
-        // very few blocks: 16-CTA clusters (non-portable size)
-        const int64_t ctas = nb * 16;
+        // fewer blocks than 2 per SM: a cluster of 8 CTAs per block (one CTA per block left
+        // 2^20-element blocks at 0.2 of peak: 64 CTAs on 148 SMs), 16 (non-portable) below
+        // SMs / 8 blocks.  CTA size: the largest of 1024 / 512 / 256 threads at which the
+        // device can hold all nb clusters at once (cudaOccupancyMaxActiveClusters: registers,
+        // GPC shape, MPS/MIG limits), so few blocks still keep enough loads in flight; if none
+        // fits in one wave, 256 (the clusters then grid-stride over the blocks).
         static const bool np = cudaFuncSetAttribute(desc::block_reduce_cluster_kernel<In, In, 16>,
                                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
-        if (np) launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 16>, (int)(nb * 16), 16, DESC_REDUCE_CLUSTER_THREADS, 0, stream, pi, po, n, B, nb, vec);
-        else launch_cluster_pdl(desc::block_reduce_cluster_kernel<In, In, 8>, (int)(nb * 8), 8, DESC_REDUCE_CLUSTER_THREADS, 0, stream, pi, po, n, B, nb, vec);
+        const bool use16 = nb * 8 < (int64_t)sms && np;
+        auto kern = use16 ? desc::block_reduce_cluster_kernel<In, In, 16>
+                          : desc::block_reduce_cluster_kernel<In, In, 8>;
+        const int CL = use16 ? 16 : 8;
+        int threads = 256;
+        for (int t : {1024, 512, 256}) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3((unsigned)(nb * CL));
+            q.blockDim = dim3(t);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = CL;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            q.attrs = at;
+            q.numAttrs = 1;
+            int active = 0;
+            if (cudaOccupancyMaxActiveClusters(&active, kern, &q) != cudaSuccess) {
+                cudaGetLastError();
+                active = 0;
+            }
+            if (active >= nb) { threads = t; break; }
+        }
+#ifdef DESC_REDUCE_CLUSTER_THREADS
+        threads = DESC_REDUCE_CLUSTER_THREADS;        // A/B builds only
+#endif
+        launch_cluster_pdl(kern, (int)(nb * CL), CL, threads, 0, stream, pi, po, n, B, nb, vec);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "block_reduce launch");

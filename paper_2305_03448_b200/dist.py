@@ -21,11 +21,13 @@ Two implementations:
   overlaps the local passes (HBM-bound).
 
 * ``PeerSlabTranspose`` -- fused peer-to-peer path: every rank maps the
-  other ranks' output slabs with CUDA IPC once; a call launches the TMA transpose kernel
-  per destination block, writing block (r, s)^T straight into out_s over NVLink -- one pass,
-  no pack/unpack, no NCCL kernels: HBM 2 S per rank (read local S, the writes of S land in
-  the peers' HBM), NVLink S (P-1)/P.  A group barrier after the kernels orders the writes
-  before anyone reads its slab.
+  other ranks' output slabs with CUDA IPC once; a call launches one transpose kernel per
+  destination block -- AUTO's kernel for its own slab, the TILED kernel (plain coalesced
+  loads of local HBM, 128-byte warp stores over NVLink; no tensor map ever addresses peer
+  memory) for the slabs on other GPUs -- writing block (r, s)^T straight into out_s: one
+  pass, no pack/unpack, no NCCL kernels: HBM 2 S per rank (read local S, the writes of S
+  land in the peers' HBM), NVLink S (P-1)/P.  A group barrier after the kernels orders the
+  writes before anyone reads its slab.
 
 The local steps are injectable (``local_transpose``/``local_copy``) only so the exchange
 logic can be tested on CPU with the gloo backend (tests/test_dist_cpu.py); the product
@@ -119,7 +121,10 @@ def slab_transpose(in_slab: torch.Tensor, out_slab: torch.Tensor | None = None, 
       the earlier ones (the NCCL collective runs on its own stream); the result does not depend
       on C.
     all_to_all: the exchange primitive (default ``torch.distributed.all_to_all_single``); an
-      injection point for the single-GPU multi-process test only."""
+      injection point for the single-GPU multi-process test only.
+    With one rank and ``chunks`` left at None the call is a single local transpose; an
+    explicit ``chunks`` runs the whole exchange pipeline even then (a one-rank NCCL
+    all-to-all is a device copy), so the NCCL code path can be exercised on one GPU."""
     P = dist.get_world_size(group) if dist.is_initialized() else 1
     r = dist.get_rank(group) if dist.is_initialized() else 0
     Rm, N = in_slab.shape
@@ -134,7 +139,7 @@ def slab_transpose(in_slab: torch.Tensor, out_slab: torch.Tensor | None = None, 
     local_transpose = local_transpose or _cuda_transpose
     local_copy = local_copy or _cuda_unpack
     all_to_all = all_to_all or dist.all_to_all_single
-    if P == 1:
+    if P == 1 and chunks is None:
         local_transpose(in_slab, out_slab)
         return out_slab
     C = default_chunks(Rm, P) if chunks is None else int(chunks)
@@ -171,7 +176,11 @@ class PeerSlabTranspose:
     (gloo in the single-GPU two-process test, NCCL in bench.py)."""
 
     def __init__(self, out_slab: torch.Tensor, M: int, group=None, kernel: str = "auto",
-                 remote_kernel: str = "tiled"):
+                 remote_kernel: str = "tiled", force_remote: bool = False):
+        """kernel: for this rank's own block; remote_kernel: for blocks stored into a slab on
+        another GPU.  force_remote: treat every peer's slab as remote even when it lives on
+        this GPU -- the one-GPU multi-process test then runs exactly the kernel selection a
+        multi-GPU run takes."""
         if not out_slab.is_cuda or not out_slab.is_contiguous():
             raise ValueError("out_slab must be a contiguous CUDA tensor")
         self.group = group
@@ -188,8 +197,8 @@ class PeerSlabTranspose:
         # blocks for a slab on ANOTHER GPU go through the TILED kernel (plain coalesced loads
         # of local HBM, 128-byte warp stores over NVLink; no tensor map ever addresses peer
         # memory); same-device slabs (the one-GPU test) take AUTO
-        self.kernels = [kernel if d == out_slab.device.index else remote_kernel
-                        for (_, _, d) in handles]
+        self.kernels = [kernel if s == self.r or (d == out_slab.device.index and not force_remote)
+                        else remote_kernel for s, (_, _, d) in enumerate(handles)]
         self.peer_ptr = []
         self._opened = []
         for s, (h, off, _) in enumerate(handles):

@@ -162,3 +162,18 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(desc, "lib_path", str(tmp_path / "nope.so"))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         desc.load()
+
+
+def test_tensor_wrappers_validate_out():
+    """block_reduce / scan hand out.data_ptr() to a C ABI that takes no output size: a wrong
+    `out` must be refused before any call."""
+    import torch
+    x = torch.zeros(100, dtype=torch.float32)
+    for bad in (torch.zeros(9, dtype=torch.float32), torch.zeros(10, dtype=torch.float64),
+                torch.zeros(20, dtype=torch.float32)[::2]):
+        with pytest.raises(ValueError, match="out must be"):
+            desc.block_reduce(x, 10, out=bad)
+    for bad in (torch.zeros(99, dtype=torch.float32), torch.zeros(100, dtype=torch.int32),
+                torch.zeros(200, dtype=torch.float32)[::2]):
+        with pytest.raises(ValueError, match="out must be"):
+            desc.scan(x, out=bad)

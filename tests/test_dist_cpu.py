@@ -70,7 +70,7 @@ def test_default_chunks_and_bad_chunks():
     assert ddist.default_chunks(8192, 8) == 4 and ddist.default_chunks(8192, 1) == 1
     assert ddist.default_chunks(256, 2) == 2 and ddist.default_chunks(100, 2) == 1
     x = torch.zeros((6, 8), dtype=torch.int32)
-    with pytest.raises(ValueError):    # P = 1 never chunks, but the out shape is still checked
+    with pytest.raises(ValueError):    # P = 1 without explicit chunks: no exchange, shape still checked
         ddist.slab_transpose(x, torch.zeros((6, 6), dtype=torch.int32))
 
 
@@ -109,7 +109,7 @@ def _worker(rank, world, port, M, N, q, chunks=None):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,M,N", [(2, 64, 96), (4, 128, 64), (2, 1024, 256)])
+@pytest.mark.parametrize("world,M,N", [(1, 64, 96), (2, 64, 96), (4, 128, 64), (2, 1024, 256)])
 def test_gloo_slab_transpose(world, M, N):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

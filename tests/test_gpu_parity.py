@@ -226,6 +226,39 @@ def test_concurrent_streams_and_graph_capture():
         assert ys[k].cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(a[k]).tobytes()
 
 
+def test_per_thread_default_streams_concurrent():
+    """Two host threads launching dynamically scheduled TMA-store transposes on the per-thread
+    default stream (the same handle, cudaStreamPerThread = 2, in both threads, but two
+    different streams): each must get its own tile counter (counters were keyed
+    by the handle), so no tile goes missing."""
+    import threading
+    R, C = 4096, 8192          # >= 16 tiles per CTA: the dynamic scheduler is on
+    a = synth.random_bits((2, R, C), 4, 12)
+    xs = [torch.from_numpy(a[k].view(np.int32)).cuda() for k in range(2)]
+    ys = [torch.zeros((C, R), dtype=torch.int32, device="cuda") for _ in range(2)]
+    torch.cuda.synchronize()
+    errs = []
+
+    def worker(k):
+        try:
+            torch.cuda.set_device(0)
+            for _ in range(20):
+                desc.desc_transpose_ex(xs[k].data_ptr(), ys[k].data_ptr(), 1, R, C, C, R, 0, 0,
+                                       "i32", "tma_st", 2)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    for k in range(2):
+        assert ys[k].cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(a[k]).tobytes()
+
+
 def test_tensor_api_dtypes():
     for dt in (torch.float32, torch.float64, torch.int32, torch.int64, torch.float16,
                torch.bfloat16, torch.uint8):
@@ -293,27 +326,45 @@ def test_config4_batched_256x1024sq_f32():
     assert y.cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(src).tobytes()
 
 
-def test_config5_65536_f32_sampled():
-    """65536 x 65536 f32 (16 GiB in + 16 GiB out) in one launch, hash-filled on device;
-    sampled 64 x 64 blocks (corners, edges, random) checked against the oracle."""
+def test_config5_65536_f32_every_element():
+    """65536 x 65536 f32 (16 GiB in + 16 GiB out, offsets beyond 2^31) in one AUTO launch,
+    hash-filled on device: ALL 2^32 output elements compared with the closed form
+    out[j][i] = H(i*N + j) (tests/fullcheck.py), plus 64 x 64 blocks at the corners and at
+    random places against the oracle itself."""
+    from tests.fullcheck import hash_transpose_mismatches
     n = 65536
     seed = synth.BASE_SEED + 5
     x = torch.empty((n, n), dtype=torch.int32, device="cuda")
     synth.hash_fill_torch(x, 0, 0, n, seed, chunk_rows=2048)
     y = torch.empty_like(x)
-    desc.transpose(x, y)
+    desc.transpose(x.view(torch.float32), y.view(torch.float32))
     torch.cuda.synchronize()
+    del x
+    torch.cuda.empty_cache()
+    bad, first = hash_transpose_mismatches(y, 0, n, seed, chunk_rows=512)
+    assert bad == 0, f"{bad} of 2^32 elements differ, first at out{first}"
     rng = np.random.default_rng(seed)
     picks = [(0, 0), (n - 64, n - 64), (0, n - 64), (n - 64, 0)] + \
-        [tuple(int(v) for v in rng.integers(0, n - 64, 2)) for _ in range(12)]
+        [tuple(int(v) for v in rng.integers(0, n - 64, 2)) for _ in range(4)]
     for i0, j0 in picks:
         ii, jj = np.meshgrid(np.arange(i0, i0 + 64), np.arange(j0, j0 + 64), indexing="ij")
         blk = synth.hash_expected_np(ii, jj, n, seed, 4)           # in[i0:i0+64, j0:j0+64]
         exp = oracle.transpose(blk)                               # -> out[j0:, i0:]
         got = y[j0:j0 + 64, i0:i0 + 64].cpu().numpy().view(np.uint32)
         assert got.tobytes() == exp.tobytes(), (i0, j0)
-    del x, y
+    del y
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("kernel", ["auto", "tma_st"])
+def test_involution_full_size(kernel):
+    """T6 at the BASELINE sizes: T(T(A)) == A bytewise for 8192^2 f32 and 3000 x 5000 f64."""
+    for shape, es, dt in (((8192, 8192), 4, torch.float32), ((3000, 5000), 8, torch.float64)):
+        a = synth.with_specials(synth.random_bits(shape, es, 31 + es), es, 5)
+        x = torch.from_numpy(a.view(NP_INT[es])).cuda().view(dt)
+        z = desc.transpose(desc.transpose(x, kernel=kernel), kernel=kernel)
+        torch.cuda.synchronize()
+        assert torch.equal(z.view(TORCH_INT[es]), x.view(TORCH_INT[es])), (shape, kernel)
 
 
 # ------------------------------------------------------------ host-buffer entry point

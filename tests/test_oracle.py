@@ -278,3 +278,30 @@ def test_pins_catch_mutants(mutant):
     decode_ok = got.shape == (cols, rows) and (i == ii).all() and (j == jj).all()
     numpy_ok = got.tobytes() == np.ascontiguousarray(a.T).tobytes()
     assert not decode_ok and not numpy_ok
+
+
+def test_fullcheck_closed_form_pinned_to_oracle():
+    """tests/fullcheck.py (the every-element check used at 65536^2) agrees with the oracle on
+    small hash-filled matrices: 0 mismatches for the oracle's transpose (whole matrix and a
+    row slab of it), exactly the planted ones otherwise, and a copy without transpose fails."""
+    import torch
+    from tests.fullcheck import hash_transpose_mismatches
+    seed = synth.BASE_SEED + 5
+    for M, N, es in ((96, 160, 4), (64, 40, 8), (1, 7, 4)):
+        x = torch.empty((M, N), dtype=torch.int32 if es == 4 else torch.int64)
+        synth.hash_fill_torch(x, 0, 0, N, seed)
+        a = x.numpy().view(synth.UINT_OF_SIZE[es])
+        ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+        assert a.tobytes() == synth.hash_expected_np(ii, jj, N, seed, es).tobytes()
+        t = oracle.transpose(a)                                  # N x M
+        y = torch.from_numpy(t.view(np.int32 if es == 4 else np.int64).copy())
+        assert hash_transpose_mismatches(y, 0, N, seed, chunk_rows=7) == (0, None)
+        r0 = N // 3
+        assert hash_transpose_mismatches(y[r0:], r0, N, seed, chunk_rows=5) == (0, None)
+        if M > 1:
+            y2 = y.clone()
+            y2[N - 1, M // 2] ^= 1 << 5
+            assert hash_transpose_mismatches(y2, 0, N, seed) == (1, (N - 1, M // 2))
+            wrong = torch.from_numpy(np.ascontiguousarray(
+                a.view(np.int32 if es == 4 else np.int64).reshape(N, M)))   # copy, no transpose
+            assert hash_transpose_mismatches(wrong, 0, N, seed)[0] > 0

@@ -50,6 +50,10 @@ def _ulp(dt, ref):
                                  # groups plus a remainder of blocks)
                                  (128 * 1000 + 128 * 7, 128), (256 * 5003, 256), (512 * 77, 512),
                                  (2048 * 33, 2048), (1024 * 301, 1024), (4000 * 300 + 7, 4000),
+                                 # 3, 5, 6 … warp rows per block (not a power of two:
+                                 # the warp-per-block kernel)
+                                 (384 * 1000, 384), (192 * 1001, 192), (1536 * 77, 1536),
+                                 (640 * 313, 640), (768 * 100, 768), (1920 * 41, 1920),
                                  # fewer blocks than CTA slots: cluster per block (ragged,
                                  # near-empty last block; more blocks than clusters)
                                  ((1 << 22) + 17, 1 << 20), (2000000, 20000),
