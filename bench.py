@@ -38,7 +38,9 @@ L2_BYTES = 126 * 1024 * 1024
 KERNEL_FN = {"tma_st": "desc::transpose_tma2_kernel (TMA load + TMA store)",
              "tma": "desc::transpose_tma_kernel (TMA load + st.global)",
              "smem": "desc::transpose_smem_kernel (32x33 smem tile)",
-             "tiled": "desc::transpose_tiled_kernel (64x65 smem tile, 16 loads in flight)"}
+             "tiled": "desc::transpose_tiled_kernel (64x65 smem tile, 16 loads in flight)",
+             "tma_tile": "desc::transpose_tma_tile_kernel (one 16 KB tile per CTA: TMA load, "
+                         "register micro-transpose, TMA store)"}
 
 WORKLOADS = {
     "8192f32": dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4,
@@ -111,11 +113,31 @@ def load_traffic(workload: str):
         return None
 
 
+_SAMPLER_CHILD = r"""
+import sys, time, json, select
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print(json.dumps({"max": pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)}), flush=True)
+out = []
+while True:
+    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    out.append((time.perf_counter(), mhz, r))
+    if select.select([sys.stdin], [], [], 0)[0]:
+        break
+    time.sleep(5e-5)
+print(json.dumps(out), flush=True)
+"""
+
+
 class ClockSampler:
     """Samples the SM clock and the throttle reasons with NVML, as fast as NVML answers, with
-    host timestamps: ``region(t0, t1)`` marks the host-time window of the timed region (from
-    just before its first event is recorded to the return of the synchronize after it), and
-    the summary reports the samples taken inside it."""
+    host timestamps (CLOCK_MONOTONIC, shared by all processes), in a CHILD PROCESS: a sampler
+    thread here would wait for the GIL while the launching thread runs, and missed the
+    1.7 ms timed region of the default line entirely.  ``region(t0, t1)`` marks the host-time
+    window of the timed region (from just before its first event is recorded to the return
+    of the synchronize after it); the summary reports the samples taken inside it."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -124,48 +146,48 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period_s: float = 0.0):
-        self.period = period_s
+    def __init__(self, index: int):
+        self.index = index
         self.samples = []            # (host time, sm MHz, reason bits)
         self.ok = False
         self.max_mhz = None
         self.t0 = self.t1 = None
         self.extended = 0
+        self.proc = None
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            import pynvml  # noqa: F401  (the child needs it)
             self.ok = True
         except Exception as e:  # pragma: no cover
             self.err = str(e)
-        self._stop = threading.Event()
-
-    def _run(self):
-        nv = self.nv
-        while not self._stop.is_set():
-            try:
-                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((time.perf_counter(), mhz, r))
-            except Exception:
-                pass
-            if self.period:
-                time.sleep(self.period)
 
     def __enter__(self):
         if self.ok:
-            self._stop = threading.Event()
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+            import subprocess
+            # NVML numbers devices physically: map the CUDA index through CUDA_VISIBLE_DEVICES
+            idx = self.index
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.index])
+                except (ValueError, IndexError):
+                    pass
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_CHILD, str(idx)],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
+            try:
+                self.max_mhz = json.loads(self.proc.stdout.readline())["max"]
+            except Exception:
+                self.ok = False
             time.sleep(0.002)        # the first samples land before the region starts
         return self
 
     def __exit__(self, *exc):
-        if self.ok:
-            self._stop.set()
-            self.t.join()
+        if self.ok and self.proc is not None:
+            out, _ = self.proc.communicate(input="stop\n", timeout=120)
+            try:
+                self.samples += [tuple(x) for x in json.loads(out.strip().splitlines()[-1])]
+            except Exception:
+                pass
+            self.proc = None
 
     def region(self, t0: float, t1: float):
         self.t0, self.t1 = t0, t1
@@ -205,12 +227,13 @@ class ClockSampler:
         out = {"sm_mhz": statistics.median(m for _, m, _ in use) if use else None,
                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
                "samples": len(self.samples), "samples_in_timed_region": len(inr),
-               "sm_mhz_from": "samples in the timed region" if inr else "all samples"}
+               "sm_mhz_from": "samples in the timed region" if inr else "all samples",
+               "sampler": "NVML polled in a child process, host CLOCK_MONOTONIC timestamps"}
         if self.extended:
             ext = [m for _, m, _ in self.samples[-self.extended:]]
             out["extension"] = {"samples": self.extended,
                                 "sm_mhz": statistics.median(ext),
-                                "what": "timed region gave < 10 NVML samples: 0.3 s of untimed "
+                                "what": "timed region gave < 10 NVML samples: untimed "
                                         "repeats of the same step right after it"}
         return out
 
@@ -1242,7 +1265,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None,
                     help="default: 8192f32 at N = 1 (configs[2], the headline target), "
                          "dist65536 at N > 1 (configs[4], the distributed transpose)")
-    ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem", "tiled"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem", "tiled", "tma_tile"],
+                    default="auto")
     ap.add_argument("--scan-algo", choices=["auto", "lookback", "three_pass", "stream"],
                     default="auto")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)

@@ -99,13 +99,19 @@ typedef enum desc_dtype {
  *   DESC_KERNEL_TMA_ST : as DESC_KERNEL_TMA, but the transposed tile is staged in
  *                      128-byte-swizzled shared memory and written with TMA bulk
  *                      tensor stores (cp.async.bulk.tensor shared->global).  Same
- *                      alignment rules; element size 4 or 8.                    */
+ *                      alignment rules; element size 4 or 8.
+ *   DESC_KERNEL_TMA_TILE : one 16 KB tile per 128-thread CTA (64x64 for 4-byte cells,
+ *                      32x64 for 8-byte cells), many CTAs per SM: TMA box loads on one
+ *                      mbarrier, conflict-free register micro-transposes written back
+ *                      into the same (swizzled) buffer, TMA bulk tensor stores.  Same
+ *                      alignment rules as DESC_KERNEL_TMA_ST; element size 4 or 8.  */
 typedef enum desc_kernel {
     DESC_KERNEL_AUTO = 0,
     DESC_KERNEL_SMEM = 1,
     DESC_KERNEL_TMA = 2,
     DESC_KERNEL_TMA_ST = 3,
-    DESC_KERNEL_TILED = 4
+    DESC_KERNEL_TILED = 4,
+    DESC_KERNEL_TMA_TILE = 5
 } desc_kernel;
 
 /* Single transpose: in (rows x cols, pitch ld_in) -> out (cols x rows, pitch ld_out). */
@@ -129,7 +135,7 @@ desc_status desc_transpose_ex(const void *in, void *out, int64_t batch,
                               desc_kernel kernel, void *stream);
 
 /* The variant AUTO would run for these arguments (no launch, no pointer
- * checks beyond alignment).  Returns DESC_KERNEL_TILED, _TMA or _TMA_ST. */
+ * checks beyond alignment).  Returns DESC_KERNEL_TILED, _TMA, _TMA_ST or _TMA_TILE. */
 desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
                                int64_t rows, int64_t cols, int64_t ld_in,
                                int64_t ld_out, int64_t stride_in,

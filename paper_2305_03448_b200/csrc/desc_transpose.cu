@@ -19,6 +19,7 @@
 #include "tiled_transpose.cuh"
 #include "tma_transpose.cuh"
 #include "tma_store_transpose.cuh"
+#include "tma_tile_transpose.cuh"
 #include "copy_kernel.cuh"
 #include "view_copy.cuh"
 #include "reduce_scan.cuh"
@@ -465,6 +466,97 @@ desc_status launch_tma2(const Args &a) {
     return DESC_OK;
 }
 
+// One tile per CTA, hardware-scheduled 1-D grid (tma_tile_transpose.cuh).  Tile order:
+// DESC_TMA_TILE_GROUP tile rows per raster group (default 1 = row-major over the tile grid,
+// like TILED; 0 = whole tile columns).
+template <int ES, int TR, int NB, int CW = 4, int TPC = 1>
+desc_status launch_tma_tile(const Args &a) {
+    using C = desc::TmaTileConfig<ES, TR, NB, CW, TPC>;
+    auto kern = desc::transpose_tma_tile_kernel<ES, TR, NB, CW, TPC>;
+    {
+        static std::mutex mu;
+        static bool opted[64] = {};
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 64 || !opted[dev]) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tma_tile smem)");
+            if (dev < 64) opted[dev] = true;
+        }
+    }
+    desc::TmaParams p;
+    p.out = a.out;
+    p.ld_out = a.ld_out;
+    p.stride_out = a.stride_out;
+    p.rows = (int32_t)a.rows;
+    p.rows_main = (int32_t)(a.rows - a.rows % (16 / a.es));
+    p.cols = (int32_t)a.cols;
+    p.batch = (int32_t)a.batch;
+    p.tiles_r = (int32_t)((a.rows + TR - 1) / TR);
+    p.tiles_c = (int32_t)((a.cols + C::TILE_COLS - 1) / C::TILE_COLS);
+    p.rank3 = a.batch > 1 ? 1 : 0;
+    p.ntiles = (int64_t)p.tiles_r * p.tiles_c * a.batch;
+    static const int grp = dev_knob("DESC_TMA_TILE_GROUP", 1);
+    p.group = grp <= 0 || grp > p.tiles_r ? p.tiles_r : grp;
+    // L2 policy of the loads: normal (evict_first costs 2-3%: with the tensor map's 256-byte
+    // L2 promotion a box row's fetch also brings the next box's row, which evict_first can
+    // drop before it is read; profiles/r02_tma_tile_sweep.txt)
+    static const int evict = dev_knob("DESC_TMA_TILE_EVICT", 0);
+    p.evict_first = evict;
+    p.sched = nullptr;
+    p.rev_rows = 0;
+    if (p.ntiles > INT32_MAX) return fail(DESC_ERR_SHAPE, "too many tiles for one launch");
+    // extra dynamic shared memory per CTA caps the resident CTAs per SM: 16 KB tiles + 20000
+    // bytes -> 6 CTAs/SM (96 KB of loads in flight) measured best; 8 (register-limited) and
+    // more lose 1-2%, 12 loses 15% (profiles/r02_tma_tile_sweep.txt)
+    static const int pad = dev_knob("DESC_TMA_TILE_SMEM_PAD", TPC == 1 && CW == 4 ? 20000 : 0);
+    const int smem = C::SMEM_BYTES + pad;
+    if (pad) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tma_tile smem pad)");
+    }
+    CUtensorMap min, mout;
+    if (desc_status s = in_map(a, TR, &min)) return s;
+    if (desc_status s = out_map(a, C::TILE_COLS, &mout)) return s;
+    cudaError_t e = launch_plain_pdl(kern, (int)((p.ntiles + TPC - 1) / TPC), C::THREADS, smem,
+                                     a.stream, min, mout, p);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "transpose_tma_tile_kernel launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
+desc_status run_tma_tile(const Args &a) {
+    static const int cfg = dev_knob("DESC_TMA_TILE_CFG", 0);   // A/B of tile shapes
+    switch (a.es) {
+        case 4:
+            switch (cfg) {
+                case 1: return launch_tma_tile<4, 128, 2>(a);   // 128 x 64, 32 KB
+                case 2: return launch_tma_tile<4, 64, 4>(a);    // 64 x 128, 32 KB
+                case 3: return launch_tma_tile<4, 32, 4>(a);    // 32 x 128, 16 KB
+                case 4: return launch_tma_tile<4, 64, 2, 8>(a);  // 8 warps
+                case 5: return launch_tma_tile<4, 64, 2, 4, 2>(a);  // 2 tiles per CTA
+                case 6: return launch_tma_tile<4, 64, 2, 8, 2>(a);
+                case 7: return launch_tma_tile<4, 32, 4, 4, 2>(a);
+                default: return launch_tma_tile<4, 64, 2>(a);   // 64 x 64 cells, 16 KB
+            }
+        case 8:
+            switch (cfg) {
+                case 1: return launch_tma_tile<8, 64, 4>(a);    // 64 x 64, 32 KB
+                case 2: return launch_tma_tile<8, 32, 8>(a);    // 32 x 128, 32 KB
+                case 3: return launch_tma_tile<8, 64, 2>(a);    // 64 x 32, 16 KB
+                case 4: return launch_tma_tile<8, 32, 4, 8>(a);
+                case 5: return launch_tma_tile<8, 32, 4, 4, 2>(a);
+                case 6: return launch_tma_tile<8, 32, 4, 8, 2>(a);
+                case 7: return launch_tma_tile<8, 64, 2, 4, 2>(a);
+                default: return launch_tma_tile<8, 32, 4>(a);   // 32 x 64 cells, 16 KB
+            }
+    }
+    return fail(DESC_ERR_KERNEL, "TMA tile kernel supports 4- and 8-byte elements only");
+}
+
 template <typename Cell>
 desc_status launch_smem(const Args &a) {
     int dev = 0;
@@ -716,6 +808,11 @@ desc_status dispatch(const Args &a, desc_kernel k) {
     if (k == DESC_KERNEL_TMA_ST && !tma_store_ok(a))
         return fail(DESC_ERR_KERNEL, "TMA-store kernel needs 4/8-byte elements and rows*size >= 16");
     if (k == DESC_KERNEL_TMA_ST) return run_tma2(a);
+    if (k == DESC_KERNEL_TMA_TILE) {
+        if (!tma_ok) return fail(DESC_ERR_KERNEL, "TMA tile kernel needs 16-byte aligned bases, ld*size and stride*size");
+        if (!tma_store_ok(a)) return fail(DESC_ERR_KERNEL, "TMA tile kernel needs 4/8-byte elements and rows*size >= 16");
+        return run_tma_tile(a);
+    }
     if (k == DESC_KERNEL_SMEM) return run_smem(a);
     if (k == DESC_KERNEL_TILED || (k == DESC_KERNEL_AUTO && (!tma_ok || tiled_preferred(a))))
         return run_tiled(a);

@@ -33,7 +33,8 @@ control listing1_race  racecheck detect --racecheck-report all
 control tiled_nosync   racecheck detect --racecheck-report all
 control rev_shared     racecheck detect --racecheck-report all
 control rev_global     racecheck clean  --racecheck-report all
-control divergent_bar  synccheck detect
+control divergent_warp synccheck detect
+control divergent_bar  synccheck clean
 control tiled_edge_oob memcheck detect
 echo "sanitizer gates: $([ $fail -eq 0 ] && echo PASS || echo FAIL)"
 exit $fail

@@ -37,7 +37,7 @@ def main():
         xin = torch.zeros((batch, rows, ld_in), dtype=TI[es], device="cuda")
         xin[:, :, :cols] = torch.from_numpy(src.view(NI[es])).cuda()
         ref = oracle.transpose(src)
-        kernels = ["smem", "tiled", "tma"] + (["tma_st"] if es in (4, 8) and rows * es >= 16 else [])
+        kernels = ["smem", "tiled", "tma"] + (["tma_st", "tma_tile"] if es in (4, 8) and rows * es >= 16 else [])
         for k in kernels:
             out = torch.zeros((batch, cols, ld_out), dtype=TI[es], device="cuda")
             desc.desc_transpose_ex(xin.data_ptr(), out.data_ptr(), batch, rows, cols, ld_in,

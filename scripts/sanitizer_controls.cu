@@ -9,8 +9,11 @@
 //     spot (expected: no report); the host index-map checker (tests/test_index_maps.py)
 //     rejects the same map.  rev_per_block_shared is the same access pattern staged in shared
 //     memory, which racecheck must report.
-//   * divergent_barrier (Sec. 2.2 "Synchronization"): `if (threadIdx.x < 32)
-//     __syncthreads();` launched with 64 threads per block; synccheck must report it.
+//   * divergent_barrier (Sec. 2.2 "Synchronization"): `if (threadIdx.x < limit)
+//     __syncthreads();`.  The paper's own case (limit 32, 64 threads per block: whole warps
+//     skip the barrier and exit) is NOT reported by synccheck on B200 -- measured: exited
+//     warps count as arrived, the kernel completes -- a second documented blind spot; with
+//     the barrier divergent INSIDE a warp (limit 16, 32 threads) synccheck must report it.
 // The Listing 1 race and the TILED kernel without its barrier are positive controls
 // too; they live in the mutant build of the product library (csrc/mutants.cuh ids 2 and 14).
 #include <cuda_runtime.h>
@@ -32,8 +35,8 @@ __global__ void rev_per_block_shared(double *array) {
     block_part[threadIdx.x] = part[threadIdx.x];
 }
 
-__global__ void divergent_barrier(int *out) {
-    if (threadIdx.x < 32) { __syncthreads(); }
+__global__ void divergent_barrier(int *out, int limit) {
+    if ((int)threadIdx.x < limit) { __syncthreads(); }
     out[blockIdx.x * blockDim.x + threadIdx.x] = (int)threadIdx.x;
 }
 
@@ -49,8 +52,8 @@ int ctl_rev_per_block(double *array, int blocks, int threads, int shared) {
     return (int)cudaDeviceSynchronize();
 }
 
-int ctl_divergent_barrier(int *out, int blocks, int threads) {
-    divergent_barrier<<<blocks, threads>>>(out);
+int ctl_divergent_barrier(int *out, int blocks, int threads, int limit) {
+    divergent_barrier<<<blocks, threads>>>(out, limit);
     return (int)cudaDeviceSynchronize();
 }
 

@@ -55,9 +55,13 @@ def test_sass_is_sm100a_with_tma(lib):
     tma = [b for b in blocks if "transpose_tma_kernel" in b[:200]]
     tma2 = [b for b in blocks if "transpose_tma2_kernel" in b[:200]]
     assert tma and tma2, "TMA kernels missing from the cubin"
-    for blk in tma + tma2:
+    tile = [b for b in blocks if "transpose_tma_tile_kernel" in b[:200]]
+    assert tile, "TMA tile kernel missing from the cubin"
+    for blk in tma + tma2 + tile:
         assert "UTMALDG" in blk, "TMA kernel does not issue cp.async.bulk.tensor loads"
         assert "SYNCS" in blk, "TMA kernel does not use mbarriers"
+    for blk in tma2 + tile:
+        assert "UTMASTG" in blk, "TMA-store kernels must store with cp.async.bulk.tensor"
     for blk in tma2:
         assert "UTMASTG" in blk, "TMA-store kernel does not issue bulk tensor stores"
 

@@ -88,7 +88,7 @@ def run_case(batch, rows, cols, es, kernel="auto", ld_in=None, ld_out=None, stri
     return sel
 
 
-KERNELS = ["auto", "smem", "tiled", "tma", "tma_st"]
+KERNELS = ["auto", "smem", "tiled", "tma", "tma_st", "tma_tile"]
 
 
 def _kernels_for(es, rows, cols, ld_in, ld_out):
@@ -96,7 +96,7 @@ def _kernels_for(es, rows, cols, ld_in, ld_out):
     if (ld_in * es) % 16 == 0 and (ld_out * es) % 16 == 0:
         ks.append("tma")
         if es in (4, 8) and rows * es >= 16:
-            ks.append("tma_st")
+            ks += ["tma_st", "tma_tile"]
     return ks
 
 
@@ -139,7 +139,7 @@ def test_tight_ld_odd_shapes_fall_back(es):
 @pytest.mark.parametrize("es", [4, 8])
 def test_padded_ld_guard_bands(es):
     """T4: 67x131 with ld_in=136, ld_out=72: padding columns and guard bands untouched."""
-    for k in ("auto", "tma", "tma_st", "smem", "tiled"):
+    for k in ("auto", "tma", "tma_st", "tma_tile", "smem", "tiled"):
         run_case(1, 67, 131, es, k, ld_in=136, ld_out=72)
 
 
@@ -148,7 +148,7 @@ def test_misaligned_base(es):
     """Base offsets that break 16-byte alignment route to the TILED kernel and stay exact."""
     assert run_case(1, 100, 200, es, in_off=es) == "tiled"
     assert run_case(1, 100, 200, es, out_off=es) == "tiled"
-    for k in ("tma", "tma_st"):
+    for k in ("tma", "tma_st", "tma_tile"):
         with pytest.raises(desc.DescError, match="DESC_ERR_KERNEL"):
             run_case(1, 100, 200, es, k, in_off=es, check=False)
 
@@ -157,7 +157,7 @@ def test_misaligned_base(es):
 def test_batched_odd_strides(es):
     """T7: 7 x (33 x 65) with strides that leave gaps; input strides overlapping allowed."""
     v = 16 // es
-    for k in ("auto", "smem", "tiled", "tma", "tma_st"):
+    for k in ("auto", "smem", "tiled", "tma", "tma_st", "tma_tile"):
         run_case(7, 33, 65, es, k, ld_in=65 + (-65) % v, ld_out=40, stride_in=33 * 72 + v,
                  stride_out=65 * 40 + 2 * v)
     run_case(5, 20, 24, es, "smem", ld_in=24, ld_out=20, stride_in=24 * 10, stride_out=480)
@@ -175,7 +175,7 @@ def test_involution_and_determinism():
     assert torch.equal(z, x)
 
 
-@pytest.mark.parametrize("kernel", ["tiled", "tma_st", "auto"])
+@pytest.mark.parametrize("kernel", ["tiled", "tma_st", "tma_tile", "auto"])
 def test_pdl_dependent_chain(kernel):
     """Back-to-back launches with programmatic dependent launch, each reading what the
     previous one wrote (no host sync in between): 24 transposes ping-ponging between two
@@ -303,7 +303,7 @@ def test_config2_8192_f32_and_i32():
     a = synth.random_bits((1, 8192, 8192), 4, synth.BASE_SEED + 2)
     x = torch.from_numpy(a[0].view(np.int32)).cuda()
     ref = oracle.transpose(a[0])
-    for k in ("auto", "tma", "tma_st", "smem", "tiled"):
+    for k in ("auto", "tma", "tma_st", "tma_tile", "smem", "tiled"):
         for dt in (torch.float32, torch.int32):
             y = desc.transpose(x.view(dt), kernel=k)
             torch.cuda.synchronize()
@@ -356,7 +356,7 @@ def test_config5_65536_f32_every_element():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("kernel", ["auto", "tma_st"])
+@pytest.mark.parametrize("kernel", ["auto", "tma_st", "tma_tile"])
 def test_involution_full_size(kernel):
     """T6 at the BASELINE sizes: T(T(A)) == A bytewise for 8192^2 f32 and 3000 x 5000 f64."""
     for shape, es, dt in (((8192, 8192), 4, torch.float32), ((3000, 5000), 8, torch.float64)):

@@ -65,6 +65,19 @@ def test_tma_store_map_is_a_race_free_bijection(es):
                 assert _check(L, shape) == [], (shape, TR, NB, CW, grid, group)
 
 
+@pytest.mark.parametrize("es", [4, 8])
+def test_tma_tile_map_is_a_race_free_bijection(es):
+    """transpose_tma_tile_kernel (csrc/tma_tile_transpose.cuh): the TMA-store kernel's lane
+    maps with 4 warps and one tile per CTA (64 x 64 for 4-byte cells: TR 64, 2 boxes; 32 x 64
+    for 8-byte cells: TR 32, 4 boxes); the transposed rows are written back into the input
+    buffer after a barrier, which the model's separate read / write intervals express."""
+    TR, NB = (64, 2) if es == 4 else (32, 4)
+    for shape in _tma_shapes(es):
+        for group in (None, 1):
+            L = IM.tma_launch(*shape, es, TR=TR, NB=NB, CW=4, grid=None, group=group)
+            assert _check(L, shape) == [], (shape, group)
+
+
 @pytest.mark.parametrize("es", [1, 2, 4, 8])
 def test_tma_load_map_is_a_race_free_bijection(es):
     """transpose_tma_kernel (TMA load + 16-byte st.global), the default configuration per
