@@ -38,7 +38,7 @@ L2_BYTES = 126 * 1024 * 1024
 KERNEL_FN = {"tma_st": "desc::transpose_tma2_kernel (TMA load + TMA store)",
              "tma": "desc::transpose_tma_kernel (TMA load + st.global)",
              "smem": "desc::transpose_smem_kernel (32x33 smem tile)",
-             "tiled": "desc::transpose_tiled_kernel (64x65 smem tile, 16 loads in flight)",
+             "tiled": "desc::transpose_tiled_kernel (64x64-cell tiles for 4-byte cells, 32x32 for 8-byte; padded smem tile, 16 / 8 loads in flight per thread)",
              "tma_tile": "desc::transpose_tma_tile_kernel (one 16 KB tile per CTA: TMA load, "
                          "register micro-transpose, TMA store)"}
 

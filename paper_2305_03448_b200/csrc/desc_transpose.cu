@@ -577,9 +577,10 @@ desc_status launch_smem(const Args &a) {
     return DESC_OK;
 }
 
-template <typename Cell>
+template <typename Cell, int TR = 0, int TC = 0, int NT = 256>
 desc_status launch_tiled(const Args &a) {
-    using C = desc::TiledCfg<Cell>;
+    using C = desc::TiledCfg<Cell, TR, TC, NT>;
+    auto kern = desc::transpose_tiled_kernel<Cell, TR, TC, NT>;
     const int64_t tiles_r = (a.rows + C::TR - 1) / C::TR, tiles_c = (a.cols + C::TC - 1) / C::TC;
     const int64_t ntiles = tiles_r * tiles_c * a.batch;
     const int64_t max_grid = (int64_t)1 << 30;           // one tile per CTA up to 2^30 tiles
@@ -592,16 +593,15 @@ desc_status launch_tiled(const Args &a) {
         if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
         std::lock_guard<std::mutex> lk(mu);
         if (dev >= 64 || !opted[dev]) {
-            e = cudaFuncSetAttribute(desc::transpose_tiled_kernel<Cell>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tiled smem)");
             if (dev < 64) opted[dev] = true;
         }
     }
-    cudaError_t e = launch_plain_pdl(desc::transpose_tiled_kernel<Cell>, grid, 256, C::SMEM,
-                                     a.stream, static_cast<const Cell *>(a.in),
-                                     static_cast<Cell *>(a.out), a.rows, a.cols, a.ld_in,
-                                     a.ld_out, a.stride_in, a.stride_out, tiles_r, tiles_c, ntiles);
+    cudaError_t e = launch_plain_pdl(kern, grid, NT, C::SMEM, a.stream,
+                                     static_cast<const Cell *>(a.in), static_cast<Cell *>(a.out),
+                                     a.rows, a.cols, a.ld_in, a.ld_out, a.stride_in, a.stride_out,
+                                     tiles_r, tiles_c, ntiles);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "transpose_tiled_kernel launch");
     g_last_launches = 1;
@@ -699,9 +699,26 @@ desc_status run_tma2(const Args &a) {
 }
 
 desc_status run_tiled(const Args &a) {
+    static const int cfg = dev_knob("DESC_TILED_CFG", 0);     // A/B of tile shapes
     switch (a.es) {
-        case 4: return launch_tiled<uint32_t>(a);
-        case 8: return launch_tiled<unsigned long long>(a);
+        case 4:
+            switch (cfg) {
+                case 1: return launch_tiled<uint32_t, 32, 64, 128>(a);
+                case 2: return launch_tiled<uint32_t, 32, 128, 256>(a);
+                case 3: return launch_tiled<uint32_t, 16, 128, 128>(a);
+                default: return launch_tiled<uint32_t>(a);
+            }
+        case 8:
+            // 32 x 32 cells, 128 threads (8 loads of 8 bytes in flight per thread, up to 16
+            // CTAs/SM): 2048^2 0.836 -> 0.852, 3000x5000 0.943 -> 0.958 of peak, 4096^2 and
+            // 8192^2 unchanged, against 32 x 64 cells with 256 threads
+            // (profiles/r02_tiled_shapes.txt)
+            switch (cfg) {
+                case 1: return launch_tiled<unsigned long long, 16, 64, 128>(a);
+                case 2: return launch_tiled<unsigned long long, 16, 128, 256>(a);
+                case 3: return launch_tiled<unsigned long long, 32, 64, 256>(a);
+                default: return launch_tiled<unsigned long long, 32, 32, 128>(a);
+            }
         case 2: return launch_tiled<uint16_t>(a);
         case 1: return launch_tiled<uint8_t>(a);
         default: return fail(DESC_ERR_DTYPE, "unsupported element size %d", a.es);

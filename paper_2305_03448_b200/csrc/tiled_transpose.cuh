@@ -39,26 +39,41 @@ namespace desc {
 #define DESC_TILED_TC4 64
 #endif
 
-template <typename Cell>
+// Tile TR x TC cells, NT threads (NW = NT/32 warps).  Loads: lane tx takes columns tx + 32g
+// (g < TC/32) of rows ty + NW*k (k < TR/NW), all issued before the first shared store.
+// Copy-out: LPR = min(TR, 32) lanes per output row, RPI = 32/LPR output rows per warp
+// instruction: lane tx writes output row oc = RPI*(ty + NW*m) + tx/LPR, column
+// orr = tx%LPR + LPR*h (each row segment = LPR cells = 128 / 256 contiguous bytes).
+template <typename Cell, int TR_ = 0, int TC_ = 0, int NT_ = 256>
 struct TiledCfg {
     static constexpr bool W8 = sizeof(Cell) == 8;
-    static constexpr int TR = W8 ? DESC_TILED_TR8 : DESC_TILED_TR4;   // tile rows (input)
-    static constexpr int TC = W8 ? DESC_TILED_TC8 : DESC_TILED_TC4;   // tile cols (input)
+    static constexpr int TR = TR_ ? TR_ : (W8 ? DESC_TILED_TR8 : DESC_TILED_TR4);   // tile rows (input)
+    static constexpr int TC = TC_ ? TC_ : (W8 ? DESC_TILED_TC8 : DESC_TILED_TC4);   // tile cols (input)
+    static constexpr int NT = NT_;                          // threads
+    static constexpr int NW = NT / 32;                      // warps
     static constexpr int CW = TC / 32;                      // column groups per lane
-    static constexpr int RK = TR / 8;                       // rows per warp
+    static constexpr int RK = TR / NW;                      // rows per warp
+    static constexpr int LPR = TR < 32 ? TR : 32;           // lanes per output row segment
+    static constexpr int RPI = 32 / LPR;                    // output rows per warp instruction
+    static constexpr int OK = TC / (RPI * NW);              // output row groups per warp
+    static constexpr int OH = TR / LPR;                     // segments per output row
     static constexpr int SMEM = TR * (TC + 1) * (int)sizeof(Cell);   // padded staging tile
+    static_assert(TC % 32 == 0 && TR % NW == 0 && TC % (RPI * NW) == 0 && 32 % LPR == 0,
+                  "tile / thread shape");
 };
 
-template <typename Cell>
-__global__ void __launch_bounds__(256)
+template <typename Cell, int TR_ = 0, int TC_ = 0, int NT_ = 256>
+__global__ void __launch_bounds__(NT_)
 transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int64_t rows,
                        int64_t cols, int64_t ld_in, int64_t ld_out, int64_t stride_in,
                        int64_t stride_out, int64_t tiles_r, int64_t tiles_c, int64_t ntiles) {
-    using C = TiledCfg<Cell>;
-    constexpr int TR = C::TR, TC = C::TC, CW = C::CW, RK = C::RK;
+    using C = TiledCfg<Cell, TR_, TC_, NT_>;
+    constexpr int TR = C::TR, TC = C::TC, CW = C::CW, RK = C::RK, NW = C::NW;
+    constexpr int LPR = C::LPR, RPI = C::RPI, OK = C::OK, OH = C::OH;
     extern __shared__ __align__(16) unsigned char tiled_smem[];
     Cell(*tile)[TC + 1] = reinterpret_cast<Cell(*)[TC + 1]>(tiled_smem);
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int ox = tx % LPR, oy = tx / LPR;                 // copy-out lane split
     // PDL: the next kernel in the stream may be scheduled into the slots our last wave
     // frees, but nothing here touches global memory before the previous grid has completed
     ptx::grid_dependency_wait();
@@ -77,11 +92,11 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
 #pragma unroll
             for (int k = 0; k < RK; ++k)
 #pragma unroll
-                for (int g = 0; g < CW; ++g) v[k][g] = src[(int64_t)(ty + 8 * k) * ld_in + tx + 32 * g];
+                for (int g = 0; g < CW; ++g) v[k][g] = src[(int64_t)(ty + NW * k) * ld_in + tx + 32 * g];
 #pragma unroll
             for (int k = 0; k < RK; ++k)
 #pragma unroll
-                for (int g = 0; g < CW; ++g) tile[ty + 8 * k][tx + 32 * g] = v[k][g];
+                for (int g = 0; g < CW; ++g) tile[ty + NW * k][tx + 32 * g] = v[k][g];
         } else {
             const int nr = (int)(rows - r0 < TR ? rows - r0 : TR);
             const int nc = (int)(cols - c0 < TC ? cols - c0 : TC);
@@ -89,26 +104,25 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
             for (int k = 0; k < RK; ++k)
 #pragma unroll
                 for (int g = 0; g < CW; ++g) {
-                    const int r = ty + 8 * k, c = tx + 32 * g;
+                    const int r = ty + NW * k, c = tx + 32 * g;
                     if (r < nr && c < nc) v[k][g] = src[(int64_t)r * ld_in + c];
                 }
 #pragma unroll
             for (int k = 0; k < RK; ++k)
 #pragma unroll
                 for (int g = 0; g < CW; ++g) {
-                    const int r = ty + 8 * k, c = tx + 32 * g;
+                    const int r = ty + NW * k, c = tx + 32 * g;
                     if (r < nr && c < nc) tile[r][c] = v[k][g];
                 }
         }
         if (!DESC_MUTANT(MUT_TILED_NO_SYNC)) __syncthreads();   // block-uniform condition
-        // copy-out: output row c0 + oc (= input column), 32 lanes x TR/32 cells contiguous
-        constexpr int OK = TC / 8, OH = TR / 32;
+        // copy-out: output row c0 + oc (= input column), LPR lanes x OH segments contiguous
         if (full) {
 #pragma unroll
             for (int m = 0; m < OK; ++m)
 #pragma unroll
                 for (int h = 0; h < OH; ++h) {
-                    const int oc = ty + 8 * m, orr = tx + 32 * h;
+                    const int oc = RPI * (ty + NW * m) + oy, orr = ox + LPR * h;
                     dst[(int64_t)oc * ld_out + orr] =
                         DESC_MUTANT(MUT_TILED_TILE_ONLY) ? tile[oc][orr] : tile[orr][oc];
                 }
@@ -119,7 +133,7 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
             for (int m = 0; m < OK; ++m)
 #pragma unroll
                 for (int h = 0; h < OH; ++h) {
-                    const int oc = ty + 8 * m, orr = tx + 32 * h;
+                    const int oc = RPI * (ty + NW * m) + oy, orr = ox + LPR * h;
                     if (oc < nc && orr < nr + (DESC_MUTANT(MUT_TILED_EDGE) ? 1 : 0))
                         dst[(int64_t)oc * ld_out + orr] =
                             DESC_MUTANT(MUT_TILED_TILE_ONLY) ? tile[oc][orr] : tile[orr][oc];

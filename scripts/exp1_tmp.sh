@@ -1,7 +1,2 @@
-# ncu A/B: TILED vs TMA tile (cfg 0, pad 20000, evict normal) on 8192^2 f32, one cold launch each
-export DESC_TMA_TILE_EVICT=0 DESC_TMA_TILE_SMEM_PAD=20000
-for k in tiled tma_tile; do
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:transpose_ -s 5 -c 1 \
-   -o gpurun_out/prof_ab_$k -f python bench.py --kernel $k --steps 8 --warmup 3 --no-oracle --no-e2e > gpurun_out/ncu_ab_$k.log 2>&1
-echo "$k rc=$?"
-done
+# small problems: transpose vs a plain row copy of the same bytes (same launch mechanics: PDL, rotating buffers)
+timeout 900 python scripts/exp_kernels.py --kernels tiled,copy,tma_tile --shapes 1024x1024:f64,2048x2048:f64,2048x4096:f64,3000x5000:f64,4096x4096:f64,8192x8192:f64,2048x2048:f32,4096x4096:f32,8192x8192:f32

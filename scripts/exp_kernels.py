@@ -41,6 +41,10 @@ def measure(kernel, batch, rows, cols, dn, K, dev):
     si, so = (rows * cols, cols * rows) if batch > 1 else (0, 0)
 
     def go(k):
+        if kernel == "copy":    # same bytes, plain 16-byte row copy (copy_rows_kernel, PDL)
+            desc.desc_copy_batched(xs[k % R].data_ptr(), ys[k % R].data_ptr(), 1, batch * rows,
+                                   cols, cols, cols, 0, 0, dn, st)
+            return
         desc.desc_transpose_ex(xs[k % R].data_ptr(), ys[k % R].data_ptr(), batch, rows, cols, cols,
                                rows, si, so, dn, kernel, st)
     for k in range(10):

@@ -115,52 +115,60 @@ def smem_hazards(L: Launch):
 
 # ------------------------------------------------------------------ TILED (AUTO's kernel)
 def tiled_cfg(es):
-    """csrc/tiled_transpose.cuh:29-50 (TiledCfg): 32 x 64 tiles for 8-byte cells, else 64 x 64."""
-    return (32, 64) if es == 8 else (64, 64)
+    """desc_transpose.cu run_tiled defaults: 32 x 32 tiles with 128 threads for 8-byte cells,
+    64 x 64 with 256 threads otherwise -> (TR, TC, NT)."""
+    return (32, 32, 128) if es == 8 else (64, 64, 256)
 
 
-def tiled_launch(batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, mutant=None):
-    """csrc/tiled_transpose.cuh:52-130 restated.  One 256-thread CTA per tile (launcher
-    desc_transpose.cu launch_tiled: grid = ntiles); mutant in {None, "tile_only" (12),
-    "edge" (13), "no_sync" (14)}."""
-    TR, TC = tiled_cfg(es)
-    RK, CW, OK, OH = TR // 8, TC // 32, TC // 8, TR // 32
+def tiled_launch(batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, mutant=None,
+                 TR=None, TC=None, NT=256):
+    """csrc/tiled_transpose.cuh transpose_tiled_kernel restated.  One NT-thread CTA per tile
+    (launcher desc_transpose.cu launch_tiled: grid = ntiles); mutant in {None, "tile_only"
+    (12), "edge" (13), "no_sync" (14)}."""
+    if TR is None:
+        TR, TC, NT = tiled_cfg(es)
+    NW = NT // 32
+    CW, RK = TC // 32, TR // NW
+    LPR = min(TR, 32)
+    RPI = 32 // LPR
+    OK, OH = TC // (RPI * NW), TR // LPR
     tiles_r, tiles_c = -(-rows // TR), -(-cols // TC)
     L = Launch()
-    tid = np.arange(256)
+    tid = np.arange(NT)
     tx, ty = tid & 31, tid >> 5
+    ox, oy = tx % LPR, tx // LPR
     k = np.arange(RK)
     g = np.arange(CW)
-    r = (ty[:, None, None] + 8 * k[None, :, None]) + 0 * g[None, None, :]      # :80 rows ty+8k
-    c = (tx[:, None, None] + 32 * g[None, None, :]) + 0 * k[None, :, None]     # cols tx+32g
+    r = (ty[:, None, None] + NW * k[None, :, None]) + 0 * g[None, None, :]     # rows ty + NW k
+    c = (tx[:, None, None] + 32 * g[None, None, :]) + 0 * k[None, :, None]     # cols tx + 32g
     th_l = np.broadcast_to(tid[:, None, None], r.shape)
     m = np.arange(OK)
     h = np.arange(OH)
-    oc = (ty[:, None, None] + 8 * m[None, :, None]) + 0 * h[None, None, :]     # :111
-    orr = (tx[:, None, None] + 32 * h[None, None, :]) + 0 * m[None, :, None]
+    oc = (RPI * (ty[:, None, None] + NW * m[None, :, None]) + oy[:, None, None]) + 0 * h[None, None, :]
+    orr = (ox[:, None, None] + LPR * h[None, None, :]) + 0 * m[None, :, None]
     th_o = np.broadcast_to(tid[:, None, None], oc.shape)
     for t in range(tiles_r * tiles_c * batch):
-        bt, rem = divmod(t, tiles_r * tiles_c)                                  # :68-71
+        bt, rem = divmod(t, tiles_r * tiles_c)
         ti, tj = divmod(rem, tiles_c)
         r0, c0 = ti * TR, tj * TC
-        full = r0 + TR <= rows and c0 + TC <= cols                             # :74
+        full = r0 + TR <= rows and c0 + TC <= cols
         nr, nc = min(rows - r0, TR), min(cols - c0, TC)
         tile = np.full((TR, TC + 1), UNWRITTEN, dtype=np.int64)
-        mask = np.ones(r.shape, bool) if full else (r < nr) & (c < nc)          # :93
+        mask = np.ones(r.shape, bool) if full else (r < nr) & (c < nc)
         src = bt * stride_in + (r0 + r) * ld_in + c0 + c
-        tile[r[mask], c[mask]] = src[mask]                                      # :84 / :100
+        tile[r[mask], c[mask]] = src[mask]
         L.sm((t, 0), th_l[mask], r[mask] * (TC + 1) + c[mask], True)
-        iv = 0 if mutant == "no_sync" else 1                                    # :103 barrier
+        iv = 0 if mutant == "no_sync" else 1                      # the staging barrier
         lim_r = nr + (1 if mutant == "edge" else 0)
-        mo = np.ones(oc.shape, bool) if full else (oc < nc) & (orr < lim_r)     # :123
-        rr, cc = (oc, orr) if mutant == "tile_only" else (orr, oc)              # :113 / :125
+        mo = np.ones(oc.shape, bool) if full else (oc < nc) & (orr < lim_r)
+        rr, cc = (oc, orr) if mutant == "tile_only" else (orr, oc)
         rr_m, cc_m = rr[mo], cc[mo]
         inb = (rr_m < TR) & (cc_m < TC + 1)
         vals = np.full(rr_m.shape, UNWRITTEN, dtype=np.int64)
         vals[inb] = tile[rr_m[inb], cc_m[inb]]
         L.unwritten_reads += int((vals == UNWRITTEN).sum())
         L.sm((t, iv), th_o[mo], rr_m * (TC + 1) + cc_m, False)
-        L.write(bt * stride_out + (c0 + oc[mo]) * ld_out + r0 + orr[mo], vals)  # :112
+        L.write(bt * stride_out + (c0 + oc[mo]) * ld_out + r0 + orr[mo], vals)
     return L
 
 

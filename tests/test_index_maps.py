@@ -33,6 +33,18 @@ def test_tiled_map_is_a_race_free_bijection(shape, es):
     assert _check(IM.tiled_launch(*shape, es), shape) == []
 
 
+# the TILED tile shapes desc_transpose.cu run_tiled can launch (DESC_TILED_CFG 1-3)
+TILED_SHAPES = {4: [(32, 64, 128), (32, 128, 256), (16, 128, 128)],
+                8: [(16, 64, 128), (16, 128, 256), (32, 64, 256)]}
+
+
+@pytest.mark.parametrize("es", [4, 8])
+@pytest.mark.parametrize("shape", SHAPES[1:4] + SHAPES[6:])
+def test_tiled_alternative_shapes_are_race_free_bijections(shape, es):
+    for TR, TC, NT in TILED_SHAPES[es]:
+        assert _check(IM.tiled_launch(*shape, es, TR=TR, TC=TC, NT=NT), shape) == [], (TR, TC, NT)
+
+
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("grid", [None, 3])
 def test_smem_map_is_a_race_free_bijection(shape, grid):
