@@ -126,7 +126,7 @@ while True:
     out.append((time.perf_counter(), mhz, r))
     if select.select([sys.stdin], [], [], 0)[0]:
         break
-    time.sleep(5e-5)
+    time.sleep(1e-4)
 print(json.dumps(out), flush=True)
 """
 
@@ -236,6 +236,20 @@ class ClockSampler:
                                 "what": "timed region gave < 10 NVML samples: untimed "
                                         "repeats of the same step right after it"}
         return out
+
+
+def host_gate(torch, stream, seconds: float):
+    """Queue a device-side spin (torch.cuda._sleep) of about `seconds` on `stream` before the
+    timed region, so that the host enqueues all K steps while the GPU is still busy: the
+    region then measures the device executing K queued steps back to back, not the host's
+    launch rate (a 2048^2 f64 step takes ~12 us on B200, about one Python + C-ABI call).
+    The spin runs BEFORE the region's first event and is not timed."""
+    torch.cuda._sleep(int(max(seconds, 1e-3) * 2.0e9))     # SM clock <= 1.965 GHz
+
+
+def gate_seconds(host_s_per_step: float, steps: int) -> float:
+    """Spin long enough to cover the host's enqueue of `steps` steps twice over (capped)."""
+    return min(5.0, 1e-3 + 2.0 * host_s_per_step * steps)
 
 
 def bench_backend():
@@ -514,10 +528,12 @@ def ours_arm(args, wl, world, rank, local):
     if kernel != "auto":
         selected = kernel
 
+    h0 = time.perf_counter()
     for _ in range(args.warmup):
         if flush:
             l2_flush()
         step()
+    host_step = (time.perf_counter() - h0) / args.warmup     # host enqueue time per step
     torch.cuda.synchronize(dev)
 
     # Timed region.  Without an L2 flush the K launches run back to back and only the two
@@ -534,7 +550,8 @@ def ours_arm(args, wl, world, rank, local):
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        t0 = time.perf_counter()
+        if not flush:
+            host_gate(torch, stream, gate_seconds(host_step, args.steps))
         region0.record(stream)
         for k in range(args.steps):
             if flush:
@@ -545,7 +562,8 @@ def ours_arm(args, wl, world, rank, local):
                 ends[k].record(stream)
         region1.record(stream)
         torch.cuda.synchronize(dev)
-        clk.region(t0, time.perf_counter())
+        t1 = time.perf_counter()
+        clk.region(t1 - region0.elapsed_time(region1) / 1e3 - 1e-4, t1)
     clk.extend(step, torch, dev)
     if world > 1:
         dist.barrier()
@@ -606,6 +624,8 @@ def ours_arm(args, wl, world, rank, local):
             "dtype": wl["dtype"], "data": "synthetic (seeded random bit patterns, host-generated)",
             "config": {"workload": wl["name"], "rows": rows, "cols": cols, "ld_in": ld_in,
                        "batch_per_gpu": batch, "kernel": selected,
+                       "queued": "the K steps are enqueued behind an untimed device spin, so the "
+                                 "region times the GPU running them back to back",
                        "parallelism": f"{world} independent replica(s), no collective",
                        "l2": ("flushed before every step (read of a 252 MiB buffer, untimed)" if flush else
                               f"{R} (input, output) pairs of {batch * mat_bytes / 1e6:.0f} MB each "
@@ -767,8 +787,10 @@ def timed_region(step, steps, warmup, dev, world):
     import torch
     import torch.distributed as dist
     stream = torch.cuda.current_stream(dev)
+    h0 = time.perf_counter()
     for _ in range(warmup):
         step()
+    host_step = (time.perf_counter() - h0) / max(warmup, 1)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -776,13 +798,14 @@ def timed_region(step, steps, warmup, dev, world):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        t0 = time.perf_counter()
+        host_gate(torch, stream, gate_seconds(host_step, steps))
         e0.record(stream)
         for _ in range(steps):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        clk.region(t0, time.perf_counter())
+        t1 = time.perf_counter()
+        clk.region(t1 - e0.elapsed_time(e1) / 1e3 - 1e-4, t1)
     if world > 1:
         dist.barrier()
     ms_max = reduce_scalar(e0.elapsed_time(e1), "max", dev)
@@ -1013,20 +1036,23 @@ def view_arm(args, wl, world, rank, local):
         desc.desc_view_copy(x.data_ptr(), y.data_ptr(), v, "f32", stream.cuda_stream)
         return desc.desc_last_launch_count()
 
+    h0 = time.perf_counter()
     for _ in range(args.warmup):
         step()
+    host_step = (time.perf_counter() - h0) / args.warmup
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
+        host_gate(torch, stream, gate_seconds(host_step, args.steps))
         e0.record(stream)
         for _ in range(args.steps):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        clk.region(t0, time.perf_counter())
+        t1 = time.perf_counter()
+        clk.region(t1 - e0.elapsed_time(e1) / 1e3 - 1e-4, t1)
     clk.extend(step, torch, dev)
     ms = e0.elapsed_time(e1)
     ms_max = reduce_scalar(ms, "max", dev)
@@ -1106,27 +1132,39 @@ def op_arm(args, wl, world, rank, local):
             desc.desc_scan_ex(x.data_ptr(), y.data_ptr(), n, wl["dtype"], work.data_ptr(), ws,
                               args.scan_algo, stream.cuda_stream)
             return desc.desc_last_launch_count()
+    h0 = time.perf_counter()
     for _ in range(args.warmup):
         step()
+    host_step = (time.perf_counter() - h0) / args.warmup
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
     launches = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
+        host_gate(torch, stream, gate_seconds(host_step, args.steps))
         e0.record(stream)
         for _ in range(args.steps):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        clk.region(t0, time.perf_counter())
+        t1 = time.perf_counter()
+        clk.region(t1 - e0.elapsed_time(e1) / 1e3 - 1e-4, t1)
     clk.extend(step, torch, dev)
     ms = e0.elapsed_time(e1)
     ms_max = reduce_scalar(ms, "max", dev)
     value = step_bytes * world * args.steps / (ms_max / 1e3) / 1e9
     achieved = step_bytes / (ms / args.steps / 1e3) / 1e9
     peak, peak_src = load_peak()
+    read_peak = None
+    if op == "reduce":
+        # the reduction reads n and writes n/B elements: its roofline is the HBM READ rate,
+        # measured here with the library's read-only probe (16-byte loads, 8 in flight, one
+        # wave) over a 1 GiB buffer, best of 20 back-to-back launches
+        read_peak = read_only_peak(torch, desc, dev, stream)
+        copy_peak, copy_src = peak, peak_src
+        peak, peak_src = read_peak, ("measured in this run: desc_read_probe over 1 GiB, 16-byte "
+                                     "ld.global.nc, 8 in flight per lane, best of 20")
     parity = cpu_baseline = None
     if rank == 0 and not args.no_oracle:
         import oracle
@@ -1171,8 +1209,9 @@ def op_arm(args, wl, world, rank, local):
                          "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(args.workload),
-                         "peak_source": peak_src + ("; read-only stream, may exceed a copy's "
-                                                    "read+write rate" if op == "reduce" else ""),
+                         "peak_source": peak_src,
+                         **({"copy_peak": copy_peak, "frac_of_copy_peak": round(achieved / copy_peak, 4),
+                             "copy_peak_source": copy_src} if op == "reduce" else {}),
                          "algorithmic_bytes_per_launch": step_bytes},
             "parity": parity, "gpu_launches": launches, "cpu_baseline": cpu_baseline, "e2e": None,
             "clocks": clk.summary(),
@@ -1181,6 +1220,25 @@ def op_arm(args, wl, world, rank, local):
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def read_only_peak(torch, desc, dev, stream, nbytes: int = 1 << 30, reps: int = 20) -> float:
+    """HBM read-only GB/s: the library's read probe over an nbytes buffer, best of `reps`
+    back-to-back launches (each timed by its own events)."""
+    buf = torch.ones(nbytes // 4, dtype=torch.int32, device=dev)
+    sink = torch.empty(desc.desc_read_probe_sink_bytes(), dtype=torch.uint8, device=dev)
+    sp = stream.cuda_stream
+    for _ in range(3):
+        desc.desc_read_probe(buf.data_ptr(), nbytes, sink.data_ptr(), sp)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record(stream)
+    for k in range(reps):
+        desc.desc_read_probe(buf.data_ptr(), nbytes, sink.data_ptr(), sp)
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    best = min(ev[k].elapsed_time(ev[k + 1]) for k in range(reps))
+    del buf, sink
+    return round(nbytes / (best / 1e3) / 1e9, 1)
 
 
 def pcie_ceiling(torch, dev, h_in, h_out, reps: int = 3) -> float:

@@ -265,6 +265,16 @@ desc_status desc_scan(const void *in, void *out, int64_t n, desc_dtype dtype, vo
 desc_status desc_scan_ex(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
                          size_t work_bytes, desc_scan_algo algo, void *stream);
 
+/* Measurement helper (not part of the method): the HBM READ-only roofline of the block-wide
+ * reduction (the reduction reads n elements and writes n/block).  Reads `bytes` bytes
+ * of device memory at `in` (16-byte aligned, bytes a multiple of 16) with 16-byte
+ * ld.global.nc loads, 8 in flight per lane, one wave of CTAs grid-striding, XOR-folds them and
+ * writes one 16-byte word per CTA to `sink` (device memory of >= desc_read_probe_sink_bytes()
+ * bytes).  Asynchronous on `stream`.  DESC_ERR_SHAPE for a misaligned base or size,
+ * DESC_ERR_NULL / DESC_ERR_MEMSPACE as elsewhere. */
+desc_status desc_read_probe(const void *in, size_t bytes, void *sink, void *stream);
+size_t desc_read_probe_sink_bytes(void);
+
 /* Recommended workspace bytes for desc_transpose_host (double-buffered 512-row bands). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);
 

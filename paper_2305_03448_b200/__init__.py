@@ -23,7 +23,7 @@ __all__ = [
     "desc_last_launch_count", "desc_copy_batched", "desc_transpose_host",
     "desc_ipc_handle", "desc_ipc_open", "desc_ipc_close", "desc_view_compile",
     "desc_view_copy", "view_copy", "desc_block_reduce", "desc_scan", "desc_scan_ex",
-    "desc_scan_workspace", "SCAN_ALGO",
+    "desc_scan_workspace", "SCAN_ALGO", "desc_read_probe", "desc_read_probe_sink_bytes",
     "block_reduce", "scan", "desc_transpose_host_workspace",
     "transpose", "transpose_batched", "transpose_host",
 ]
@@ -113,6 +113,10 @@ def load():
     lib.desc_scan.restype = ci
     lib.desc_scan_ex.argtypes = [vp, vp, i64, ci, vp, ctypes.c_size_t, ci, vp]
     lib.desc_scan_ex.restype = ci
+    lib.desc_read_probe.argtypes = [vp, ctypes.c_size_t, vp, vp]
+    lib.desc_read_probe.restype = ci
+    lib.desc_read_probe_sink_bytes.argtypes = []
+    lib.desc_read_probe_sink_bytes.restype = ctypes.c_size_t
     lib.desc_last_launch_count.argtypes = []
     lib.desc_last_launch_count.restype = ci
     lib.desc_status_string.argtypes = [ci]
@@ -259,6 +263,15 @@ def scan(x, out=None, work=None, algo="auto"):
     desc_scan_ex(x.data_ptr(), out.data_ptr(), x.numel(), x.dtype, work.data_ptr(), work.numel(),
                  algo, _stream_of(x))
     return out
+
+
+def desc_read_probe(in_ptr, nbytes, sink_ptr, stream=0):
+    """Measurement helper: read nbytes at in_ptr (the reduction's read roofline)."""
+    return _check(load().desc_read_probe(in_ptr, nbytes, sink_ptr, stream))
+
+
+def desc_read_probe_sink_bytes() -> int:
+    return load().desc_read_probe_sink_bytes()
 
 
 IPC_HANDLE_BYTES = 64

@@ -1639,6 +1639,31 @@ desc_status run_scan(const void *in, void *out, int64_t n, desc_dtype dtype, voi
 
 extern "C" {
 
+size_t desc_read_probe_sink_bytes(void) { return 16 * 8 * 1024; }   // <= 8 CTAs/SM x 1024 SMs
+
+desc_status desc_read_probe(const void *in, size_t bytes, void *sink, void *stream) {
+    g_last_launches = 0;
+    if (!in || !sink) return fail(DESC_ERR_NULL, "null pointer");
+    if (reinterpret_cast<uintptr_t>(in) % 16 || bytes % 16)
+        return fail(DESC_ERR_SHAPE, "read probe needs a 16-byte aligned base and size");
+    if (bytes == 0) return DESC_OK;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (desc_status st = check_memspace(in, dev, "in")) return st;
+    if (desc_status st = check_memspace(sink, dev, "sink")) return st;
+    DevInfo di;
+    if (desc_status st = device_info(dev, &di)) return st;
+    const int grid = di.sms * 8 < 8 * 1024 ? di.sms * 8 : 8 * 1024;   // one wave, 8 CTAs/SM
+    e = launch_plain_pdl(desc::read_probe_kernel, grid, 256, 0, static_cast<cudaStream_t>(stream),
+                         static_cast<const uint4 *>(in), (int64_t)(bytes / 16),
+                         static_cast<uint4 *>(sink));
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "read_probe launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
 desc_status desc_block_reduce(const void *in, void *out, int64_t n, int64_t block,
                               desc_dtype dtype, void *stream) {
     return run_reduce(in, out, n, block, dtype, static_cast<cudaStream_t>(stream));

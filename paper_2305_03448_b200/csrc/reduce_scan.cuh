@@ -306,6 +306,47 @@ block_reduce_cluster_kernel(const In *__restrict__ in, Out *__restrict__ out, in
     }
 }
 
+// ---- read-only HBM probe (measurement helper: the reduction's read roofline) --------------
+// One wave of 256-thread CTAs grid-striding over 16-byte vectors, 8 loads in flight per lane,
+// XOR-folded; one 16-byte word per CTA is written so the loads cannot be elided.
+__global__ void __launch_bounds__(256) read_probe_kernel(const uint4 *__restrict__ in, int64_t nv,
+                                                         uint4 *__restrict__ sink) {
+    ptx::grid_dependency_wait();
+    ptx::grid_launch_dependents();
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 7 * stride < nv; i += 8 * stride) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_nc_v4(in + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            acc.x ^= v[u].x; acc.y ^= v[u].y; acc.z ^= v[u].z; acc.w ^= v[u].w;
+        }
+    }
+    for (; i < nv; i += stride) {
+        const uint4 v = ld_nc_v4(in + i);
+        acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, o);
+        acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, o);
+    }
+    __shared__ uint4 part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint4 t = part[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) { t.x ^= part[w].x; t.y ^= part[w].y; t.z ^= part[w].z; t.w ^= part[w].w; }
+        sink[blockIdx.x] = t;
+    }
+}
+
 // ---- scan ---------------------------------------------------------------------------------
 // Tile descriptors of the single-pass scans are 64-bit words {value bits : 32, status : 32}
 // (status 0 = not ready, 1 = aggregate A, 2 = inclusive prefix P), written and read with

@@ -129,11 +129,9 @@ def test_scan_stream_many_tiles_per_cta(dt):
 
 @pytest.mark.parametrize("algo", ["lookback", "three_pass", "stream"])
 def test_scan_f32_special_values(algo):
-    """f32 widening to the fp64 accumulator: the streaming scan converts normal numbers and
-    +-0 on the integer pipe and everything else with the conversion instruction, per 16-byte
-    vector -- mixed vectors of +-0, subnormals, the extreme normal exponents and ordinary
-    values must still meet the bound; an inf makes every later prefix inf, a NaN every later
-    prefix NaN, exactly as in the oracle."""
+    """f32 widening to the fp64 accumulator: mixed vectors of +-0, subnormals, the extreme
+    normal exponents and ordinary values must still meet the bound; an inf makes every later
+    prefix inf, a NaN every later prefix NaN, exactly as in the oracle."""
     n = (1 << 22) + 5
     rng = np.random.default_rng(7)
     a = synth.random_floats(n, np.float32, 8)
@@ -196,3 +194,19 @@ def test_errors():
     big = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
     with pytest.raises(desc.DescError, match="KERNEL"):
         desc.desc_scan_ex(y.data_ptr(), y.data_ptr(), 100, "f32", big.data_ptr(), 1 << 20, 9)
+
+
+def test_read_probe_reads_every_byte():
+    """desc_read_probe (the reduction's read-roofline helper): the XOR of the per-CTA sink words
+    equals the XOR of every 16-byte word of the input, so every byte was loaded."""
+    for nbytes in (16, 16 * 1001, 1 << 24):
+        a = synth.random_bits((nbytes // 4,), 4, nbytes).view(np.int32)
+        x = torch.from_numpy(a).cuda()
+        sink = torch.zeros(desc.desc_read_probe_sink_bytes(), dtype=torch.uint8, device="cuda")
+        desc.desc_read_probe(x.data_ptr(), nbytes, sink.data_ptr())
+        torch.cuda.synchronize()
+        got = np.bitwise_xor.reduce(sink.cpu().numpy().view(np.uint32).reshape(-1, 4), axis=0)
+        exp = np.bitwise_xor.reduce(a.view(np.uint32).reshape(-1, 4), axis=0)
+        assert got.tobytes() == exp.tobytes(), nbytes
+    with pytest.raises(desc.DescError, match="SHAPE"):
+        desc.desc_read_probe(x.data_ptr() + 4, 16, sink.data_ptr())
