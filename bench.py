@@ -956,8 +956,9 @@ def dist_arm(args, wl, world, rank, local):
                 "impl": other, "value": round(r["value"], 2), "unit": "GB/s",
                 "ms_per_step": round(r["ms"] / args.steps, 4), "roofline": r["roofline"],
                 "parity": r["parity"], "gpu_launches": r["launches"], "chunks": r["chunks"],
-                "what": ("fused transpose + exchange: one kernel per destination writes block "
-                         "(r,s)^T straight into rank s's slab through CUDA IPC (2S HBM per rank)"
+                "what": ("fused transpose + exchange: ONE kernel per step "
+                         "(desc_slab_transpose_peer) writes block (r,s)^T straight into every "
+                         "rank s's slab through CUDA IPC (2S HBM per rank, no NCCL kernels)"
                          if other == "p2p" else "NCCL all-to-all path")}
         except Exception as e:  # noqa: BLE001  (reported, the headline stays)
             extra["exchange_" + other] = {"error": f"{type(e).__name__}: {e}"[:300]}

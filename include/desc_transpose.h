@@ -265,6 +265,25 @@ desc_status desc_scan(const void *in, void *out, int64_t n, desc_dtype dtype, vo
 desc_status desc_scan_ex(const void *in, void *out, int64_t n, desc_dtype dtype, void *d_work,
                          size_t work_bytes, desc_scan_algo algo, void *stream);
 
+/* Fused transpose + exchange of the distributed slab transpose (BASELINE north_star (4);
+ * SURVEY.md 8(f) NEXT #1; reading R13) in ONE launch.  The global M x N matrix is
+ * held as row slabs: this rank r of P owns input rows [r*Rm, (r+1)*Rm), Rm = M/P, as in_slab
+ * (Rm x N, row pitch N); rank s owns output rows [s*Rn, (s+1)*Rn) of the N x M transpose,
+ * Rn = N/P, as out_slabs[s] (Rn x M, pitch M) -- this rank's own slab, or another rank's slab
+ * mapped into this process (desc_ipc_open; same device or a peer device this one can access).
+ * Writes block (r, s)^T = (in_slab[:, s*Rn : (s+1)*Rn])^T into columns [r*Rm, (r+1)*Rm) of
+ * out_slabs[s] for every s: one TILED launch whose tiles pick their destination slab, so the
+ * local transpose and every rank's NVLink stores run in the same kernel (2S HBM per rank, no
+ * pack / unpack, no NCCL kernels).  Only this rank's column blocks are written.
+ * 1 <= P <= 8, 0 <= r < P, P | M, P | N, Rn a multiple of the tile width (64 cells for 4-byte,
+ * 32 for 8-byte types), else DESC_ERR_SHAPE; 4/8-byte dtypes only (DESC_ERR_DTYPE); in_slab
+ * overlapping an out slab gives DESC_ERR_ALIAS.  Asynchronous on `stream`; it does NOT order
+ * the ranks: the caller completes every rank's call (e.g. a group barrier after the stream)
+ * before any rank reads its slab. */
+desc_status desc_slab_transpose_peer(const void *in_slab, void *const *out_slabs, int32_t P,
+                                     int32_t r, int64_t M, int64_t N, desc_dtype dtype,
+                                     void *stream);
+
 /* Measurement helper (not part of the method): the HBM READ-only roofline of the block-wide
  * reduction (the reduction reads n elements and writes n/block).  Reads `bytes` bytes
  * of device memory at `in` (16-byte aligned, bytes a multiple of 16) with 16-byte

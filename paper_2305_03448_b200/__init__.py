@@ -24,6 +24,7 @@ __all__ = [
     "desc_ipc_handle", "desc_ipc_open", "desc_ipc_close", "desc_view_compile",
     "desc_view_copy", "view_copy", "desc_block_reduce", "desc_scan", "desc_scan_ex",
     "desc_scan_workspace", "SCAN_ALGO", "desc_read_probe", "desc_read_probe_sink_bytes",
+    "desc_slab_transpose_peer",
     "block_reduce", "scan", "desc_transpose_host_workspace",
     "transpose", "transpose_batched", "transpose_host",
 ]
@@ -113,6 +114,9 @@ def load():
     lib.desc_scan.restype = ci
     lib.desc_scan_ex.argtypes = [vp, vp, i64, ci, vp, ctypes.c_size_t, ci, vp]
     lib.desc_scan_ex.restype = ci
+    lib.desc_slab_transpose_peer.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                             ctypes.c_int32, i64, i64, ci, vp]
+    lib.desc_slab_transpose_peer.restype = ci
     lib.desc_read_probe.argtypes = [vp, ctypes.c_size_t, vp, vp]
     lib.desc_read_probe.restype = ci
     lib.desc_read_probe_sink_bytes.argtypes = []
@@ -263,6 +267,13 @@ def scan(x, out=None, work=None, algo="auto"):
     desc_scan_ex(x.data_ptr(), out.data_ptr(), x.numel(), x.dtype, work.data_ptr(), work.numel(),
                  algo, _stream_of(x))
     return out
+
+
+def desc_slab_transpose_peer(in_ptr, out_ptrs, r, M, N, dtype, stream=0):
+    """One launch: block (r, s)^T of this rank's slab into every out_ptrs[s] (see the header)."""
+    P = len(out_ptrs)
+    arr = (ctypes.c_void_p * max(P, 1))(*out_ptrs)
+    return _check(load().desc_slab_transpose_peer(in_ptr, arr, P, r, M, N, _dt(dtype), stream))
 
 
 def desc_read_probe(in_ptr, nbytes, sink_ptr, stream=0):

@@ -577,10 +577,13 @@ desc_status launch_smem(const Args &a) {
     return DESC_OK;
 }
 
-template <typename Cell, int TR = 0, int TC = 0, int NT = 256>
-desc_status launch_tiled(const Args &a) {
+template <typename Cell, int TR = 0, int TC = 0, int NT = 256, bool SCATTER = false>
+desc_status launch_tiled(const Args &a, const desc::TiledScatter *scatter = nullptr) {
     using C = desc::TiledCfg<Cell, TR, TC, NT>;
-    auto kern = desc::transpose_tiled_kernel<Cell, TR, TC, NT>;
+    auto kern = desc::transpose_tiled_kernel<Cell, TR, TC, NT, SCATTER>;
+    desc::TiledScatter sc;
+    memset(&sc, 0, sizeof sc);
+    if (scatter) sc = *scatter;
     const int64_t tiles_r = (a.rows + C::TR - 1) / C::TR, tiles_c = (a.cols + C::TC - 1) / C::TC;
     const int64_t ntiles = tiles_r * tiles_c * a.batch;
     const int64_t max_grid = (int64_t)1 << 30;           // one tile per CTA up to 2^30 tiles
@@ -601,7 +604,7 @@ desc_status launch_tiled(const Args &a) {
     cudaError_t e = launch_plain_pdl(kern, grid, NT, C::SMEM, a.stream,
                                      static_cast<const Cell *>(a.in), static_cast<Cell *>(a.out),
                                      a.rows, a.cols, a.ld_in, a.ld_out, a.stride_in, a.stride_out,
-                                     tiles_r, tiles_c, ntiles);
+                                     tiles_r, tiles_c, ntiles, sc);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "transpose_tiled_kernel launch");
     g_last_launches = 1;
@@ -1635,9 +1638,56 @@ desc_status run_scan(const void *in, void *out, int64_t n, desc_dtype dtype, voi
     }
 }
 
+// ---- fused transpose + exchange: one launch for every destination slab ------------------
+desc_status run_slab_peer(const void *in, void *const *outs, int32_t P, int32_t r, int64_t M,
+                          int64_t N, int es, cudaStream_t stream) {
+    g_last_launches = 0;
+    if (es != 4 && es != 8) return fail(DESC_ERR_DTYPE, "peer slab transpose supports 4- and 8-byte cells");
+    if (!in || !outs) return fail(DESC_ERR_NULL, "null pointer");
+    if (P < 1 || P > desc::kMaxScatter || r < 0 || r >= P)
+        return fail(DESC_ERR_SHAPE, "need 1 <= P <= %d and 0 <= r < P (P=%d r=%d)", desc::kMaxScatter, P, r);
+    if (M <= 0 || N <= 0 || M % P || N % P)
+        return fail(DESC_ERR_SHAPE, "M=%lld and N=%lld must be positive multiples of P=%d (R13)",
+                    (long long)M, (long long)N, P);
+    const int64_t Rm = M / P, Rn = N / P;
+    const int tc = es == 8 ? 32 : 64;                     // TILED tile width (cells)
+    if (Rn % tc)
+        return fail(DESC_ERR_SHAPE, "N/P = %lld must be a multiple of the %d-cell tile width", (long long)Rn, tc);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (desc_status st = check_memspace(in, dev, "in_slab")) return st;
+    desc::TiledScatter sc;
+    memset(&sc, 0, sizeof sc);
+    int64_t in_bytes, out_bytes;
+    if (!mul_ok(Rm * N, es, &in_bytes) || !mul_ok(Rn * M, es, &out_bytes))
+        return fail(DESC_ERR_SHAPE, "extent overflows int64");
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(in);
+    for (int s = 0; s < P; ++s) {
+        if (!outs[s]) return fail(DESC_ERR_NULL, "out_slabs[%d] is null", s);
+        if (desc_status st = check_memspace(outs[s], dev, "out_slabs[s]")) return st;
+        const uintptr_t o0 = reinterpret_cast<uintptr_t>(outs[s]);
+        if (i0 < o0 + (uintptr_t)out_bytes && o0 < i0 + (uintptr_t)in_bytes)
+            return fail(DESC_ERR_ALIAS, "in_slab and out_slabs[%d] overlap (&uniq, P:576-579)", s);
+        sc.dst[s] = outs[s];
+    }
+    sc.seg = Rn;
+    sc.col_off = r * Rm;
+    Args a{in, outs[r], 1, Rm, N, N, M, 0, 0, es, stream};
+    return es == 8 ? launch_tiled<unsigned long long, 32, 32, 128, true>(a, &sc)
+                   : launch_tiled<uint32_t, 64, 64, 256, true>(a, &sc);
+}
+
 }  // namespace
 
 extern "C" {
+
+desc_status desc_slab_transpose_peer(const void *in_slab, void *const *out_slabs, int32_t P,
+                                     int32_t r, int64_t M, int64_t N, desc_dtype dtype,
+                                     void *stream) {
+    return run_slab_peer(in_slab, out_slabs, P, r, M, N, dtype_size(dtype),
+                         static_cast<cudaStream_t>(stream));
+}
 
 size_t desc_read_probe_sink_bytes(void) { return 16 * 8 * 1024; }   // <= 8 CTAs/SM x 1024 SMs
 

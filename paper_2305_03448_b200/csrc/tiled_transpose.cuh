@@ -62,11 +62,23 @@ struct TiledCfg {
                   "tile / thread shape");
 };
 
-template <typename Cell, int TR_ = 0, int TC_ = 0, int NT_ = 256>
+// Scatter destinations of the fused peer-to-peer slab transpose (desc_slab_transpose_peer):
+// input column c goes to destination s = c / seg, at column (c - s*seg) of that destination's
+// rows, output column offset col_off (rank r's block of every destination slab).  seg is a
+// multiple of the tile width, so a tile never straddles two destinations.
+constexpr int kMaxScatter = 8;
+struct TiledScatter {
+    void *dst[kMaxScatter];
+    int64_t seg;
+    int64_t col_off;
+};
+
+template <typename Cell, int TR_ = 0, int TC_ = 0, int NT_ = 256, bool SCATTER = false>
 __global__ void __launch_bounds__(NT_)
 transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int64_t rows,
                        int64_t cols, int64_t ld_in, int64_t ld_out, int64_t stride_in,
-                       int64_t stride_out, int64_t tiles_r, int64_t tiles_c, int64_t ntiles) {
+                       int64_t stride_out, int64_t tiles_r, int64_t tiles_c, int64_t ntiles,
+                       const __grid_constant__ TiledScatter sc) {
     using C = TiledCfg<Cell, TR_, TC_, NT_>;
     constexpr int TR = C::TR, TC = C::TC, CW = C::CW, RK = C::RK, NW = C::NW;
     constexpr int LPR = C::LPR, RPI = C::RPI, OK = C::OK, OH = C::OH;
@@ -85,7 +97,13 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
         const int64_t ti = rem / tiles_c, tj = rem - ti * tiles_c;
         const int64_t r0 = ti * TR, c0 = tj * TC;
         const Cell *src = in + bt * stride_in + r0 * ld_in + c0;
-        Cell *dst = out + bt * stride_out + c0 * ld_out + r0;
+        Cell *dst;
+        if constexpr (SCATTER) {              // block (r, s)^T lands in destination s
+            const int64_t sd = c0 / sc.seg;
+            dst = static_cast<Cell *>(sc.dst[sd]) + (c0 - sd * sc.seg) * ld_out + sc.col_off + r0;
+        } else {
+            dst = out + bt * stride_out + c0 * ld_out + r0;
+        }
         const bool full = r0 + TR <= rows && c0 + TC <= cols;
         Cell v[RK][CW];
         if (full) {

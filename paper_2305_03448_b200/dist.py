@@ -21,11 +21,12 @@ Two implementations:
   overlaps the local passes (HBM-bound).
 
 * ``PeerSlabTranspose`` -- fused peer-to-peer path: every rank maps the
-  other ranks' output slabs with CUDA IPC once; a call launches one transpose kernel per
-  destination block -- AUTO's kernel for its own slab, the TILED kernel (plain coalesced
-  loads of local HBM, 128-byte warp stores over NVLink; no tensor map ever addresses peer
-  memory) for the slabs on other GPUs -- writing block (r, s)^T straight into out_s: one
-  pass, no pack/unpack, no NCCL kernels: HBM 2 S per rank (read local S, the writes of S
+  other ranks' output slabs with CUDA IPC once; a call is ONE launch
+  (desc_slab_transpose_peer): TILED tiles (plain coalesced loads of local HBM, 128-byte warp
+  stores, over NVLink for the other GPUs' slabs; no tensor map ever addresses peer memory)
+  that each pick their destination slab, writing block (r, s)^T straight into out_s (shapes
+  the fused kernel cannot tile fall back to one launch per destination): one pass, no
+  pack/unpack, no NCCL kernels: HBM 2 S per rank (read local S, the writes of S
   land in the peers' HBM), NVLink S (P-1)/P.  A group barrier after the kernels orders the
   writes before anyone reads its slab.
 
@@ -176,8 +177,11 @@ class PeerSlabTranspose:
     (gloo in the single-GPU two-process test, NCCL in bench.py)."""
 
     def __init__(self, out_slab: torch.Tensor, M: int, group=None, kernel: str = "auto",
-                 remote_kernel: str = "tiled", force_remote: bool = False):
-        """kernel: for this rank's own block; remote_kernel: for blocks stored into a slab on
+                 remote_kernel: str = "tiled", force_remote: bool = False, fused: bool = True):
+        """fused: ONE launch for all destinations (desc_slab_transpose_peer: TILED tiles that
+        pick their destination slab) when P <= 8 and N/P is a multiple of the tile width;
+        otherwise one launch per destination with
+        kernel: for this rank's own block; remote_kernel: for blocks stored into a slab on
         another GPU.  force_remote: treat every peer's slab as remote even when it lives on
         this GPU -- the one-GPU multi-process test then runs exactly the kernel selection a
         multi-GPU run takes."""
@@ -199,6 +203,9 @@ class PeerSlabTranspose:
         # memory); same-device slabs (the one-GPU test) take AUTO
         self.kernels = [kernel if s == self.r or (d == out_slab.device.index and not force_remote)
                         else remote_kernel for s, (_, _, d) in enumerate(handles)]
+        es = out_slab.element_size()
+        tile_w = 32 if es == 8 else 64
+        self.fused = bool(fused and self.P <= 8 and es in (4, 8) and self.lay.Rn % tile_w == 0)
         self.peer_ptr = []
         self._opened = []
         for s, (h, off, _) in enumerate(handles):
@@ -219,8 +226,12 @@ class PeerSlabTranspose:
         if barrier:       # every peer finished reading its previous output
             dist.barrier(group=self.group)
         launches = 0
+        if self.fused:
+            desc.desc_slab_transpose_peer(in_slab.data_ptr(), self.peer_ptr, self.r, lay.M, lay.N,
+                                          in_slab.dtype, stream)
+            launches = desc.desc_last_launch_count()
         # start with the next rank so that the P writers spread over the P destinations
-        for k in range(self.P):
+        for k in range(0 if self.fused else self.P):
             s = (self.r + k) % self.P
             src = in_slab.data_ptr() + s * lay.Rn * es                       # block (r, s)
             dst = self.peer_ptr[s] + self.r * lay.Rm * es                    # out_s[:, r*Rm]

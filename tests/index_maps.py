@@ -416,3 +416,30 @@ def view_thread_cells(shape, ops):
     `ops` (one element per thread, in the view's row-major order) accesses: the view's
     index array from the oracle's definitions (oracle/views.py)."""
     return V.index_view(shape, ops).ravel()
+
+
+def slab_peer_launches(P, M, N, es, TR=None, TC=None, NT=256):
+    """desc_slab_transpose_peer (csrc/desc_transpose.cu run_slab_peer + the SCATTER branch of
+    csrc/tiled_transpose.cuh) restated for every rank r of P: rank r's TILED launch over its
+    Rm x N slab, each tile routed to destination s = c0 / Rn at column (c - s*Rn), output
+    column offset r*Rm.  Returns {s: (dst offsets in slab s, global input ids)} over all
+    ranks, plus the number of tiles whose columns straddle two destinations."""
+    if TR is None:
+        TR, TC, NT = tiled_cfg(es)
+    Rm, Rn = M // P, N // P
+    per = {s: ([], []) for s in range(P)}
+    straddle = 0
+    for r in range(P):
+        L = tiled_launch(1, Rm, N, N, M, 0, 0, es, TR=TR, TC=TC, NT=NT)
+        d = np.concatenate(L.dst)
+        v = np.concatenate(L.val)
+        c, row = d // M, d % M                     # unscattered: out[c][row], c = input column
+        c0 = (c // TC) * TC                         # the tile's first column
+        s_tile = c0 // Rn                           # destination the kernel picks (per tile)
+        straddle += int((s_tile != c // Rn).sum())
+        gid = v + r * Rm * N                        # local ids -> global input ids
+        for s in range(P):
+            m = s_tile == s
+            per[s][0].append((c[m] - s * Rn) * M + r * Rm + row[m])
+            per[s][1].append(gid[m])
+    return {s: (np.concatenate(a), np.concatenate(b)) for s, (a, b) in per.items()}, straddle

@@ -181,3 +181,19 @@ def test_tensor_wrappers_validate_out():
                 torch.zeros(200, dtype=torch.float32)[::2]):
         with pytest.raises(ValueError, match="out must be"):
             desc.scan(x, out=bad)
+
+
+def test_slab_peer_validation_codes(lib):
+    """desc_slab_transpose_peer argument checks (all before any CUDA call)."""
+    import ctypes
+    f = lib.desc_slab_transpose_peer
+    outs = (ctypes.c_void_p * 2)(FAKE_OUT, FAKE_OUT + (1 << 30))
+    assert f(None, outs, 2, 0, 256, 256, 0, None) == 1                 # null in_slab
+    assert f(FAKE_IN, None, 2, 0, 256, 256, 0, None) == 1              # null out array
+    assert f(FAKE_IN, outs, 0, 0, 256, 256, 0, None) == 2              # P < 1
+    assert f(FAKE_IN, outs, 9, 0, 256, 256, 0, None) == 2              # P > 8
+    assert f(FAKE_IN, outs, 2, 2, 256, 256, 0, None) == 2              # r >= P
+    assert f(FAKE_IN, outs, 2, 0, 255, 256, 0, None) == 2              # P does not divide M
+    assert f(FAKE_IN, outs, 2, 0, 256, 96, 0, None) == 2               # N/P = 48: not tile-wide
+    assert "tile width" in desc.desc_last_error()
+    assert f(FAKE_IN, outs, 2, 0, 256, 256, 4, None) == 3              # 2-byte cells

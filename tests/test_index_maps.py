@@ -216,3 +216,27 @@ def test_group_by_tile_blocks_own_disjoint_parts():
             assert (owner[cells] == -1).all()
             owner[cells] = bi * 4 + bj
     assert (owner >= 0).all()
+
+
+@pytest.mark.parametrize("P,M,N,es", [(2, 128, 256, 4), (4, 96, 512, 4), (8, 64, 512, 8),
+                                      (2, 70, 128, 8), (3, 90, 192, 4)])
+def test_slab_peer_scatter_covers_every_slab_exactly_once(P, M, N, es):
+    """desc_slab_transpose_peer over all P ranks: the union of the P launches writes every
+    element of every rank's output slab exactly once, with the global transpose's source
+    (out_s[j][i] = A[i][s*Rn + j]), and no tile straddles two destinations when N/P is a
+    multiple of the tile width (the C ABI rejects other shapes)."""
+    Rm, Rn = M // P, N // P
+    per, straddle = IM.slab_peer_launches(P, M, N, es)
+    assert straddle == 0
+    for s in range(P):
+        dst, gid = per[s]
+        assert np.array_equal(np.sort(dst), np.arange(Rn * M)), s          # exactly once
+        j, i = dst // M, dst % M
+        assert np.array_equal(gid, i * N + s * Rn + j), s                  # the transpose
+
+
+def test_slab_peer_scatter_needs_tile_aligned_segments():
+    """Why the C ABI requires N/P to be a multiple of the tile width: with N/P = 48 and 64-wide
+    tiles, tiles straddle two destination slabs and the per-tile routing misplaces columns."""
+    per, straddle = IM.slab_peer_launches(2, 64, 96, 4)
+    assert straddle > 0
