@@ -52,11 +52,17 @@ for st in "$@"; do
           > gpurun_out/launches_bench.log 2>&1
       echo "launches rc=$?";;
     ncu:*)
+      # summarised ON THE BOX (reports are ~12 MB each and gpurun copies back <= 64 MiB):
+      # gpurun_out/ncu_<w>_<k>.md + the traffic entry in gpurun_out/ncu_traffic.json;
+      # KEEP_REP=1 keeps the .ncu-rep too
       rest=${st#ncu:}; w=${rest%%:*}; k=${rest#*:}
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 5 -c 1 \
           -o gpurun_out/prof_${w}_${k} -f python bench.py --workload $w --steps 8 --warmup 3 \
           --no-oracle --no-e2e > gpurun_out/ncu_${w}_${k}.log 2>&1
-      echo "ncu $w $k rc=$?";;
+      echo "ncu $w $k rc=$?"
+      python scripts/ncu_summary.py gpurun_out/prof_${w}_${k}.ncu-rep gpurun_out/ncu_${w}_${k}.md $w > /dev/null 2>&1
+      cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
+      [ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/prof_${w}_${k}.ncu-rep;;
     exp:*)
       timeout 1200 python scripts/${st#exp:} > gpurun_out/exp.log 2>&1
       echo "exp ${st#exp:} rc=$?"; tail -40 gpurun_out/exp.log;;
