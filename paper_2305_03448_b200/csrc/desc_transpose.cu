@@ -601,10 +601,34 @@ desc_status launch_tiled(const Args &a, const desc::TiledScatter *scatter = null
             if (dev < 64) opted[dev] = true;
         }
     }
+    // L2 prefetch of each CTA's tile before griddepcontrol.wait (tiled_transpose.cuh).  Every
+    // CTA prefetches (mode 2, default): same box, back to back (profiles/r02_tiled_prefetch.txt)
+    // 8192^2 f32 1.000 -> 1.023, 4096^2 f32 0.933 -> 0.999, 2048^2 f64 0.870 -> 0.980,
+    // 3000x5000 f64 0.957 -> 0.997 of the copy peak; only the first wave (mode 1, the CTAs that
+    // can be resident while the previous grid runs) recovers the launch ramp but not the
+    // extra loads in flight of the later CTAs.  DESC_TILED_PF=0/1/2 for A/B.
+    static int64_t pf_slots[64] = {};
+    static const int pf_mode = dev_knob("DESC_TILED_PF", 2);   // 0 off, 1 first wave, 2 all
+    int64_t pf_ctas = 0;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && pf_slots[dev] == 0) {
+            DevInfo di;
+            if (desc_status st = device_info(dev, &di)) return st;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, C::SMEM) != cudaSuccess) {
+                cudaGetLastError();
+                occ = 1;
+            }
+            pf_slots[dev] = (int64_t)di.sms * (occ > 0 ? occ : 1);
+        }
+        pf_ctas = pf_mode == 0 ? 0 : pf_mode == 2 ? ((int64_t)1 << 62) : (dev < 64 ? pf_slots[dev] : 0);
+    }
     cudaError_t e = launch_plain_pdl(kern, grid, NT, C::SMEM, a.stream,
                                      static_cast<const Cell *>(a.in), static_cast<Cell *>(a.out),
                                      a.rows, a.cols, a.ld_in, a.ld_out, a.stride_in, a.stride_out,
-                                     tiles_r, tiles_c, ntiles, sc);
+                                     tiles_r, tiles_c, ntiles, pf_ctas, sc);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "transpose_tiled_kernel launch");
     g_last_launches = 1;

@@ -79,6 +79,13 @@ __device__ __forceinline__ void grid_launch_dependents() {
 }
 
 // ---- TMA -------------------------------------------------------------------
+// Prefetch the 128-byte line at p into L2 (no data returned to the SM; non-faulting).  Safe
+// BEFORE griddepcontrol.wait: L2 is the GPU's point of coherence, so a line a prerequisite
+// grid still writes is updated in L2, and loads after the wait see its final value.
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

@@ -38,6 +38,9 @@ namespace desc {
 #ifndef DESC_TILED_TC4
 #define DESC_TILED_TC4 64
 #endif
+#ifndef DESC_TILED_L2PF          // L2 prefetch of the first tile before griddepcontrol.wait
+#define DESC_TILED_L2PF 1
+#endif
 
 // Tile TR x TC cells, NT threads (NW = NT/32 warps).  Loads: lane tx takes columns tx + 32g
 // (g < TC/32) of rows ty + NW*k (k < TR/NW), all issued before the first shared store.
@@ -73,12 +76,18 @@ struct TiledScatter {
     int64_t col_off;
 };
 
+// Register budget: 256-thread CTAs keep 5 resident per SM (<= 51 registers; the L2
+// prefetch block would otherwise push the 4-byte kernel to 62 registers = 4 CTAs/SM and cost
+// 3-4% at 8192^2); 128-thread CTAs: DESC_TILED_MINB128 (A/B; 0 = no constraint, 56 regs).
+#ifndef DESC_TILED_MINB128
+#define DESC_TILED_MINB128 0
+#endif
 template <typename Cell, int TR_ = 0, int TC_ = 0, int NT_ = 256, bool SCATTER = false>
-__global__ void __launch_bounds__(NT_)
+__global__ void __launch_bounds__(NT_, NT_ >= 256 ? 5 : DESC_TILED_MINB128)
 transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int64_t rows,
                        int64_t cols, int64_t ld_in, int64_t ld_out, int64_t stride_in,
                        int64_t stride_out, int64_t tiles_r, int64_t tiles_c, int64_t ntiles,
-                       const __grid_constant__ TiledScatter sc) {
+                       int64_t pf_ctas, const __grid_constant__ TiledScatter sc) {
     using C = TiledCfg<Cell, TR_, TC_, NT_>;
     constexpr int TR = C::TR, TC = C::TC, CW = C::CW, RK = C::RK, NW = C::NW;
     constexpr int LPR = C::LPR, RPI = C::RPI, OK = C::OK, OH = C::OH;
@@ -86,15 +95,40 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
     Cell(*tile)[TC + 1] = reinterpret_cast<Cell(*)[TC + 1]>(tiled_smem);
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int ox = tx % LPR, oy = tx / LPR;                 // copy-out lane split
+    const int64_t tiles_per_mat = tiles_r * tiles_c;
+    // this CTA's first tile (computed once: used by the prefetch and the first iteration)
+    int64_t t = blockIdx.x;
+    int64_t bt = t / tiles_per_mat;
+    int64_t ti = (t - bt * tiles_per_mat) / tiles_c;
+    int64_t tj = t - bt * tiles_per_mat - ti * tiles_c;
+#if DESC_TILED_L2PF
+    // While a previous grid may still run (PDL), warm L2 with this CTA's first input tile:
+    // one prefetch per 128-byte line of its rows, no data to the SM, no ordering needed --
+    // L2 is the point of coherence, so lines a previous grid still writes stay correct for
+    // the loads after griddepcontrol.wait.  Hides the ramp of a back-to-back launch behind
+    // the previous launch's tail, and puts the whole tile's requests in flight at once --
+    // more than the registers of the cell loads below can hold.  pf_ctas
+    // limits it to the first pf_ctas CTAs (desc_transpose.cu launch_tiled: all by default).
+    {
+        constexpr int LPRow = (TC * (int)sizeof(Cell) + 127) / 128;    // lines per tile row
+        if (t < pf_ctas && t < ntiles && (int)threadIdx.x < TR * LPRow) {
+            const int r = threadIdx.x / LPRow, l = threadIdx.x % LPRow;
+            const int64_t row = ti * TR + r, col = tj * TC + l * (128 / (int)sizeof(Cell));
+            if (row < rows && col < cols)
+                ptx::prefetch_l2(in + bt * stride_in + row * ld_in + col);
+        }
+    }
+#endif
     // PDL: the next kernel in the stream may be scheduled into the slots our last wave
     // frees, but nothing here touches global memory before the previous grid has completed
     ptx::grid_dependency_wait();
     ptx::grid_launch_dependents();
-    const int64_t tiles_per_mat = tiles_r * tiles_c;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t bt = t / tiles_per_mat;
-        const int64_t rem = t - bt * tiles_per_mat;
-        const int64_t ti = rem / tiles_c, tj = rem - ti * tiles_c;
+    for (; t < ntiles; t += gridDim.x) {
+        if (t != (int64_t)blockIdx.x) {
+            bt = t / tiles_per_mat;
+            ti = (t - bt * tiles_per_mat) / tiles_c;
+            tj = t - bt * tiles_per_mat - ti * tiles_c;
+        }
         const int64_t r0 = ti * TR, c0 = tj * TC;
         const Cell *src = in + bt * stride_in + r0 * ld_in + c0;
         Cell *dst;
