@@ -59,6 +59,10 @@ struct TmaTileConfig {
     static_assert(TR <= 256 && TILE_COLS <= 256, "TMA box dimension <= 256");
 };
 
+#ifndef DESC_TMA_TILE_PF      // L2 prefetch of the CTA's boxes before griddepcontrol.wait
+#define DESC_TMA_TILE_PF 1
+#endif
+
 // minimum resident CTAs per SM the register allocation must allow (A/B builds; 0 = none:
 // ~62 registers, 8 CTAs/SM)
 #ifndef DESC_TMA_TILE_MINB
@@ -83,13 +87,30 @@ transpose_tma_tile_kernel(const __grid_constant__ CUtensorMap map_in,
         for (int i = 0; i < TPC; ++i) ptx::mbar_init(ptx::smem_u32(&full_bar[i]), 1);
         ptx::fence_mbarrier_init();
     }
+    const int64_t t0 = (int64_t)blockIdx.x * TPC;
+#if DESC_TMA_TILE_PF
+    // L2 prefetch of this CTA's boxes before griddepcontrol.wait (as in the TILED kernel:
+    // L2 is the point of coherence, so this is safe while a previous grid still runs)
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tensormap(&map_in);
+        for (int i = 0; i < TPC; ++i) {
+            if (t0 + i >= p.ntiles) break;
+            const TileCoord tc = tile_coords(t0 + i, p);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+                const int32_t c0 = tc.tj * C::TILE_COLS + nb * C::TC;
+                if (p.rank3) ptx::tma_prefetch_3d(&map_in, c0, tc.ti * TR, (int32_t)tc.bt);
+                else ptx::tma_prefetch_2d(&map_in, c0, tc.ti * TR);
+            }
+        }
+    }
+#endif
     __syncthreads();
     // PDL: the prologue may overlap the previous kernel's tail; no global access before
     // every prerequisite grid has completed.
     ptx::grid_dependency_wait();
     ptx::grid_launch_dependents();
 
-    const int64_t t0 = (int64_t)blockIdx.x * TPC;
     if (threadIdx.x == 0) {
         ptx::prefetch_tensormap(&map_in);
         ptx::prefetch_tensormap(&map_out);
