@@ -1159,13 +1159,15 @@ def op_arm(args, wl, world, rank, local):
     peak, peak_src = load_peak()
     read_peak = None
     if op == "reduce":
-        # the reduction reads n and writes n/B elements: its roofline is the HBM READ rate,
-        # measured here with the library's read-only probe (16-byte loads, 8 in flight, one
-        # wave) over a 1 GiB buffer, best of 20 back-to-back launches
+        # the reduction reads n and writes n/B elements: its roofline is the HBM READ rate.
+        # A plain read-only probe (desc_read_probe: 16-byte loads, 8 in flight per lane, 4 KB
+        # per warp, 1 GiB, best of 20) is measured in this run, but the
+        # reduction's L2 prefetch of the next chunk reads faster than that probe, so the
+        # roofline peak is the nominal HBM3e rate (an upper bound); the probe is reported beside
         read_peak = read_only_peak(torch, desc, dev, stream)
         copy_peak, copy_src = peak, peak_src
-        peak, peak_src = read_peak, ("measured in this run: desc_read_probe over 1 GiB, 16-byte "
-                                     "ld.global.nc, 8 in flight per lane, best of 20")
+        peak, peak_src = NOMINAL_HBM_GBS, ("nominal B200 HBM3e 8 TB/s (BASELINE.json north star): "
+                                           "an upper bound for a read-only stream")
     parity = cpu_baseline = None
     if rank == 0 and not args.no_oracle:
         import oracle
@@ -1211,7 +1213,11 @@ def op_arm(args, wl, world, rank, local):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(args.workload),
                          "peak_source": peak_src,
-                         **({"copy_peak": copy_peak, "frac_of_copy_peak": round(achieved / copy_peak, 4),
+                         **({"read_probe": read_peak,
+                             "frac_of_read_probe": round(achieved / read_peak, 4),
+                             "read_probe_what": "desc_read_probe in this run: plain 16-byte "
+                                                "ld.global.nc, 8 in flight per lane, 1 GiB, best of 20",
+                             "copy_peak": copy_peak, "frac_of_copy_peak": round(achieved / copy_peak, 4),
                              "copy_peak_source": copy_src} if op == "reduce" else {}),
                          "algorithmic_bytes_per_launch": step_bytes},
             "parity": parity, "gpu_launches": launches, "cpu_baseline": cpu_baseline, "e2e": None,

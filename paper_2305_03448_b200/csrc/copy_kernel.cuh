@@ -20,6 +20,18 @@ __global__ void __launch_bounds__(256)
 copy_rows_kernel(const char *__restrict__ in, char *__restrict__ out, int64_t rows,
                  int64_t total_rows, int64_t units, int64_t ld_in_b, int64_t ld_out_b,
                  int64_t stride_in_b, int64_t stride_out_b) {
+    // The CTA's first row into L2 before the dependency wait (as in the TILED transpose: L2
+    // is the point of coherence): 2048^2 f64-sized copies 0.79 -> 1.02 of the copy peak back
+    // to back.  Prefetching the NEXT row inside the loop loses (0.96 -> 0.84 at 256 MB): with
+    // writes in flight the prefetched lines are evicted before use
+    // (profiles/r02_reduce_prefetch.txt).
+    if ((int64_t)blockIdx.x < total_rows) {
+        const int64_t b = blockIdx.x / rows, i = blockIdx.x - b * rows;
+        const char *src = in + b * stride_in_b + i * ld_in_b;
+        const int64_t bytes = units * (int64_t)sizeof(V);
+        for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += (int64_t)blockDim.x * 128)
+            ptx::prefetch_l2(src + o);
+    }
     ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
     ptx::grid_launch_dependents();
     for (int64_t r = blockIdx.x; r < total_rows; r += gridDim.x) {

@@ -1713,7 +1713,7 @@ desc_status desc_slab_transpose_peer(const void *in_slab, void *const *out_slabs
                          static_cast<cudaStream_t>(stream));
 }
 
-size_t desc_read_probe_sink_bytes(void) { return 16 * 8 * 1024; }   // <= 8 CTAs/SM x 1024 SMs
+size_t desc_read_probe_sink_bytes(void) { return 16 * 8 * 1024; }   // one word per CTA, <= 8192 CTAs
 
 desc_status desc_read_probe(const void *in, size_t bytes, void *sink, void *stream) {
     g_last_launches = 0;
@@ -1728,7 +1728,8 @@ desc_status desc_read_probe(const void *in, size_t bytes, void *sink, void *stre
     if (desc_status st = check_memspace(sink, dev, "sink")) return st;
     DevInfo di;
     if (desc_status st = device_info(dev, &di)) return st;
-    const int grid = di.sms * 8 < 8 * 1024 ? di.sms * 8 : 8 * 1024;   // one wave, 8 CTAs/SM
+    const int grid = di.sms * 16 < 8 * 1024 ? di.sms * 16 : 8 * 1024;  // 16 x 256 threads/SM
+                                                                         // (as the reduction)
     e = launch_plain_pdl(desc::read_probe_kernel, grid, 256, 0, static_cast<cudaStream_t>(stream),
                          static_cast<const uint4 *>(in), (int64_t)(bytes / 16),
                          static_cast<uint4 *>(sink));

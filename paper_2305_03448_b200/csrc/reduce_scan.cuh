@@ -80,6 +80,13 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void *p) {
     return r;
 }
 
+#ifndef DESC_REDUCE_L2PF       // warp-row kernel: L2 prefetch of the first work item before
+#define DESC_REDUCE_L2PF 2      // griddepcontrol.wait (1), and of the next one inside the loop (2)
+#endif
+#ifndef DESC_PROBE_PF          // read probe: L2 prefetch one chunk ahead (A/B only: costs the
+#define DESC_PROBE_PF 0         // tight probe loop 15%, profiles/r02_reduce_prefetch.txt)
+#endif
+
 // 16-byte loads in flight per lane in the reduction's body loop
 #ifndef DESC_REDUCE_UNROLL
 #define DESC_REDUCE_UNROLL 8
@@ -155,16 +162,35 @@ block_reduce_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t n,
 template <typename In, typename Out, int P, int L = 8>
 __global__ void __launch_bounds__(256)
 block_reduce_rows_kernel(const In *__restrict__ in, Out *__restrict__ out, int64_t nblocks) {
-    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
-    ptx::grid_launch_dependents();
     using Acc = typename AccOf<In>::T;
     constexpr int K = L / P;           // blocks per warp iteration, L loads in flight per lane
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const uint4 *vp = reinterpret_cast<const uint4 *>(in);
     const int64_t full = nblocks / K * K;   // the rest go through the per-block loop below
+#if DESC_REDUCE_L2PF
+    {   // the warp's first K blocks into L2 before the dependency wait (as in the TILED
+        // transpose: L2 is the point of coherence; one prefetch per 128-byte line)
+        const int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32 * K;
+        if (b0 < full && (lane & 7) == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int p = 0; p < P; ++p) ptx::prefetch_l2(vp + ((b0 + k) * P + p) * 32 + lane);
+    }
+#endif
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
     for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32 * K; b0 < full;
          b0 += warps * K) {
+#if DESC_REDUCE_L2PF >= 2
+        if ((lane & 7) == 0 && b0 + warps * K < full)
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    ptx::prefetch_l2(vp + ((b0 + warps * K + k) * P + p) * 32 + lane);
+#endif
         uint4 v[K][P];
 #pragma unroll
         for (int k = 0; k < K; ++k)
@@ -307,25 +333,36 @@ block_reduce_cluster_kernel(const In *__restrict__ in, Out *__restrict__ out, in
 }
 
 // ---- read-only HBM probe (measurement helper: the reduction's read roofline) --------------
-// One wave of 256-thread CTAs grid-striding over 16-byte vectors, 8 loads in flight per lane,
-// XOR-folded; one 16-byte word per CTA is written so the loads cannot be elided.
+// A plain read-only stream: each warp reads 4 KB contiguous chunks (8 x 512-byte rows, one
+// 16-byte load per lane per row, all 8 in flight) grid-striding over the buffer, 16 CTAs of
+// 256 threads per SM.  XOR-folded; one 16-byte word per CTA is written so the loads cannot
+// be elided.  (The reduction itself, with its L2 prefetch of the next chunk, reads faster:
+// the probe context, not the ceiling; bench.py reports both against the nominal HBM3e rate.)
 __global__ void __launch_bounds__(256) read_probe_kernel(const uint4 *__restrict__ in, int64_t nv,
                                                          uint4 *__restrict__ sink) {
     ptx::grid_dependency_wait();
     ptx::grid_launch_dependents();
     uint4 acc = make_uint4(0, 0, 0, 0);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + 7 * stride < nv; i += 8 * stride) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t nchunks = nv / 256;                      // 256 vectors = 4 KB per chunk
+    for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; c < nchunks; c += warps) {
+#if DESC_PROBE_PF
+        if ((lane & 7) == 0 && c + warps < nchunks)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ptx::prefetch_l2(in + (c + warps) * 256 + u * 32 + lane);
+#endif
         uint4 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = ld_nc_v4(in + i + u * stride);
+        for (int u = 0; u < 8; ++u) v[u] = ld_nc_v4(in + c * 256 + u * 32 + lane);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             acc.x ^= v[u].x; acc.y ^= v[u].y; acc.z ^= v[u].z; acc.w ^= v[u].w;
         }
     }
-    for (; i < nv; i += stride) {
+    // ragged tail (< 4 KB): the first warp of the grid
+    for (int64_t i = nchunks * 256 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv;
+         i += (int64_t)gridDim.x * blockDim.x) {
         const uint4 v = ld_nc_v4(in + i);
         acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
     }
