@@ -733,6 +733,9 @@ desc_status run_tiled(const Args &a) {
                 case 1: return launch_tiled<uint32_t, 32, 64, 128>(a);
                 case 2: return launch_tiled<uint32_t, 32, 128, 256>(a);
                 case 3: return launch_tiled<uint32_t, 16, 128, 128>(a);
+                case 4: return launch_tiled<uint32_t, 32, 32, 128>(a);
+                case 5: return launch_tiled<uint32_t, 64, 32, 128>(a);
+                case 6: return launch_tiled<uint32_t, 64, 128, 256>(a);
                 default: return launch_tiled<uint32_t>(a);
             }
         case 8:
@@ -744,6 +747,9 @@ desc_status run_tiled(const Args &a) {
                 case 1: return launch_tiled<unsigned long long, 16, 64, 128>(a);
                 case 2: return launch_tiled<unsigned long long, 16, 128, 256>(a);
                 case 3: return launch_tiled<unsigned long long, 32, 64, 256>(a);
+                case 4: return launch_tiled<unsigned long long, 64, 32, 128>(a);
+                case 5: return launch_tiled<unsigned long long, 32, 64, 128>(a);
+                case 6: return launch_tiled<unsigned long long, 64, 64, 256>(a);
                 default: return launch_tiled<unsigned long long, 32, 32, 128>(a);
             }
         case 2: return launch_tiled<uint16_t>(a);
