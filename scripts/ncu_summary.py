@@ -117,6 +117,10 @@ def summarize_launches(path, out_md):
         v = float(r[idx["Metric Value"]].replace(",", "")) * scale[r[idx["Metric Unit"]]]
         agg[r[idx["Kernel Name"]]][0] += 1
         agg[r[idx["Kernel Name"]]][1] += v
+    # bench.py's untimed device spin (torch.cuda._sleep, queued before the timed region so the
+    # region times the GPU, not the host's launches) is not part of a step: listed apart
+    gate = {k: v for k, v in agg.items() if "spin_kernel" in k}
+    agg = {k: v for k, v in agg.items() if "spin_kernel" not in k}
     tot = sum(t for _, t in agg.values())
     lines = [f"# Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`): "
              f"`{os.path.basename(path)}`", "",
@@ -124,6 +128,10 @@ def summarize_launches(path, out_md):
              "| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"| `{k[:90]}` | {n} | {t:.1f} | {100 * t / tot:.1f}% | {t / n:.2f} |")
+    for k, (n, t) in gate.items():
+        lines += ["", f"Not in a step: `{k[:60]}` x{n} ({t:.0f} us) -- bench.py's untimed device "
+                      "spin before the timed region (its length follows the host's launch time, "
+                      "which ncu inflates)."]
     with open(out_md, "w") as f:
         f.write("\n".join(lines) + "\n")
     print(open(out_md).read())
