@@ -40,7 +40,9 @@ KERNEL_FN = {"tma_st": "desc::transpose_tma2_kernel (TMA load + TMA store)",
              "smem": "desc::transpose_smem_kernel (32x33 smem tile)",
              "tiled": "desc::transpose_tiled_kernel (64x64-cell tiles for 4-byte cells, 32x32 for 8-byte; padded smem tile, 16 / 8 loads in flight per thread)",
              "tma_tile": "desc::transpose_tma_tile_kernel (one 16 KB tile per CTA: TMA load, "
-                         "register micro-transpose, TMA store)"}
+                         "register micro-transpose, TMA store)",
+             "vtiled": "desc::transpose_vtiled_kernel (one tile per CTA: 16-byte cp.async staging "
+                       "into a 16-byte-swizzled tile, register micro-transposes, 16-byte stores)"}
 
 WORKLOADS = {
     "8192f32": dict(batch=1, rows=8192, cols=8192, dtype="f32", es=4,
@@ -100,14 +102,15 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(workload: str):
+def load_traffic(workload: str, kernel: str = "auto"):
     """dram bytes (read+write) per launch of the dominant kernel from the committed
-    `ncu --set full` summary, if one exists for this workload."""
+    `ncu --set full` summary, if one exists for this workload (and, for an explicit
+    --kernel, for that kernel: key "<workload>:<kernel>")."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        v = d.get(workload)
+        v = d.get(workload if kernel in ("auto", None) else f"{workload}:{kernel}")
         return None if v is None else float(v["dram_bytes_per_launch"])
     except Exception:
         return None
@@ -640,7 +643,7 @@ def ours_arm(args, wl, world, rank, local):
                          "nominal_peak": NOMINAL_HBM_GBS,
                          "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": load_traffic(args.workload), "peak_source": peak_src,
+                         "traffic": load_traffic(args.workload, args.kernel), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes,
                          "kernel": KERNEL_FN[selected],
                          "launch_ms_mean_in_region": round(avg_launch_ms, 5),
@@ -1330,7 +1333,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None,
                     help="default: 8192f32 at N = 1 (configs[2], the headline target), "
                          "dist65536 at N > 1 (configs[4], the distributed transpose)")
-    ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem", "tiled", "tma_tile"],
+    ap.add_argument("--kernel", choices=["auto", "tma", "tma_st", "smem", "tiled", "tma_tile", "vtiled"],
                     default="auto")
     ap.add_argument("--scan-algo", choices=["auto", "lookback", "three_pass", "stream"],
                     default="auto")

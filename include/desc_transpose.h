@@ -104,14 +104,21 @@ typedef enum desc_dtype {
  *                      32x64 for 8-byte cells), many CTAs per SM: TMA box loads on one
  *                      mbarrier, conflict-free register micro-transposes written back
  *                      into the same (swizzled) buffer, TMA bulk tensor stores.  Same
- *                      alignment rules as DESC_KERNEL_TMA_ST; element size 4 or 8.  */
+ *                      alignment rules as DESC_KERNEL_TMA_ST; element size 4 or 8.
+ *   DESC_KERNEL_VTILED : one tile per CTA (64x64 cells for 4-byte, 32x32 for 8-byte cells)
+ *                      staged with 16-byte cp.async copies into a 16-byte XOR-swizzled
+ *                      shared tile (conflict-free both ways, no padding), 4x4 / 2x2
+ *                      register micro-transposes, 16-byte coalesced stores.  Needs the
+ *                      TMA alignment rules above plus rows and cols multiples of 16/size;
+ *                      element size 4 or 8.  */
 typedef enum desc_kernel {
     DESC_KERNEL_AUTO = 0,
     DESC_KERNEL_SMEM = 1,
     DESC_KERNEL_TMA = 2,
     DESC_KERNEL_TMA_ST = 3,
     DESC_KERNEL_TILED = 4,
-    DESC_KERNEL_TMA_TILE = 5
+    DESC_KERNEL_TMA_TILE = 5,
+    DESC_KERNEL_VTILED = 6
 } desc_kernel;
 
 /* Single transpose: in (rows x cols, pitch ld_in) -> out (cols x rows, pitch ld_out). */

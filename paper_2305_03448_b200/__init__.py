@@ -37,7 +37,7 @@ lib_path = os.environ.get("DESC_LIB") or os.path.join(_PKG, "libdesc_transpose.s
 STATUS = {0: "DESC_OK", 1: "DESC_ERR_NULL", 2: "DESC_ERR_SHAPE", 3: "DESC_ERR_DTYPE",
           4: "DESC_ERR_ALIAS", 5: "DESC_ERR_MEMSPACE", 6: "DESC_ERR_CUDA", 7: "DESC_ERR_KERNEL"}
 DTYPE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3, "f16": 4, "bf16": 5, "u8": 6}
-KERNEL = {"auto": 0, "smem": 1, "tma": 2, "tma_st": 3, "tiled": 4, "tma_tile": 5}
+KERNEL = {"auto": 0, "smem": 1, "tma": 2, "tma_st": 3, "tiled": 4, "tma_tile": 5, "vtiled": 6}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 SCAN_ALGO = {"auto": 0, "lookback": 1, "three_pass": 2, "stream": 3}
 

@@ -20,6 +20,7 @@
 #include "tma_transpose.cuh"
 #include "tma_store_transpose.cuh"
 #include "tma_tile_transpose.cuh"
+#include "vtiled_transpose.cuh"
 #include "copy_kernel.cuh"
 #include "view_copy.cuh"
 #include "reduce_scan.cuh"
@@ -557,6 +558,65 @@ desc_status run_tma_tile(const Args &a) {
     return fail(DESC_ERR_KERNEL, "TMA tile kernel supports 4- and 8-byte elements only");
 }
 
+// 16-byte-vector tile kernel (vtiled_transpose.cuh): 4/8-byte cells, the TMA alignment rules
+// (16-byte bases, ld*size and stride*size multiples of 16) and rows, cols multiples of the
+// cells per 16-byte chunk, so edge tiles hold whole chunks and micro-blocks.
+bool vtiled_ok(const Args &a) {
+    if ((a.es != 4 && a.es != 8) || a.rev_rows || !tma_eligible(a)) return false;
+    const int64_t vec = 16 / a.es;
+    return a.rows % vec == 0 && a.cols % vec == 0;
+}
+
+template <int ES, int TCH, int NT>
+desc_status launch_vtiled(const Args &a) {
+    using C = desc::VTiledCfg<ES, TCH, NT>;
+    auto kern = desc::transpose_vtiled_kernel<ES, TCH, NT>;
+    const int64_t tiles_r = (a.rows + C::TR - 1) / C::TR, tiles_c = (a.cols + C::TC - 1) / C::TC;
+    const int64_t ntiles = tiles_r * tiles_c * a.batch;
+    const int64_t max_grid = (int64_t)1 << 30;
+    const int grid = (int)(ntiles < max_grid ? ntiles : max_grid);
+    static_assert(C::SMEM <= 48 * 1024, "vtiled tile fits the default shared-memory window");
+    cudaError_t e = launch_plain_pdl(kern, grid, NT, C::SMEM, a.stream,
+                                     static_cast<const char *>(a.in), static_cast<char *>(a.out),
+                                     a.rows, a.cols, a.ld_in, a.ld_out, a.stride_in, a.stride_out,
+                                     tiles_r, tiles_c, ntiles);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "transpose_vtiled_kernel launch");
+    g_last_launches = 1;
+    return DESC_OK;
+}
+
+desc_status run_vtiled(const Args &a) {
+    // Tile shapes swept on B200 (profiles/r02_vtiled_ab.txt, back to back, frac of the copy
+    // peak): 4-byte cells 64 x 64 with 128 threads (8 copies in flight each; 8192^2 1.023-1.025,
+    // 256 threads 0.982), 8-byte cells 32 x 32 with 64 threads (8 copies each; 3000x5000
+    // 0.996-0.998, 8192^2 1.033).  DESC_VTILED_CFG=<n> for A/B.
+    static const int cfg = dev_knob("DESC_VTILED_CFG", 0);
+    switch (a.es) {
+        case 4:
+            switch (cfg) {
+                case 1: return launch_vtiled<4, 16, 256>(a);    // 64 x 64, 4 copies / thread
+                case 2: return launch_vtiled<4, 32, 256>(a);    // 64 x 128, 32 KB
+                case 3: return launch_vtiled<4, 8, 128>(a);     // 64 x 32, 8 KB
+                case 4: return launch_vtiled<4, 16, 64>(a);     // 64 x 64, 16 copies / thread
+                case 5: return launch_vtiled<4, 32, 128>(a);    // 64 x 128, 16 copies / thread
+                case 6: return launch_vtiled<4, 8, 64>(a);      // 64 x 32, 8 copies / thread
+                default: return launch_vtiled<4, 16, 128>(a);   // 64 x 64 cells, 16 KB
+            }
+        case 8:
+            switch (cfg) {
+                case 1: return launch_vtiled<8, 16, 256>(a);    // 32 x 32, 2 copies / thread
+                case 2: return launch_vtiled<8, 32, 256>(a);    // 32 x 64, 16 KB
+                case 3: return launch_vtiled<8, 8, 128>(a);     // 32 x 16, 4 KB
+                case 4: return launch_vtiled<8, 16, 128>(a);    // 32 x 32, 4 copies / thread
+                case 5: return launch_vtiled<8, 32, 128>(a);    // 32 x 64, 8 copies / thread
+                case 6: return launch_vtiled<8, 32, 64>(a);     // 32 x 64, 16 copies / thread
+                default: return launch_vtiled<8, 16, 64>(a);    // 32 x 32 cells, 8 KB
+            }
+    }
+    return fail(DESC_ERR_KERNEL, "vector tile kernel supports 4- and 8-byte elements only");
+}
+
 template <typename Cell>
 desc_status launch_smem(const Args &a) {
     int dev = 0;
@@ -862,6 +922,12 @@ desc_status dispatch(const Args &a, desc_kernel k) {
         if (!tma_ok) return fail(DESC_ERR_KERNEL, "TMA tile kernel needs 16-byte aligned bases, ld*size and stride*size");
         if (!tma_store_ok(a)) return fail(DESC_ERR_KERNEL, "TMA tile kernel needs 4/8-byte elements and rows*size >= 16");
         return run_tma_tile(a);
+    }
+    if (k == DESC_KERNEL_VTILED) {
+        if (!vtiled_ok(a))
+            return fail(DESC_ERR_KERNEL, "vector tile kernel needs 4/8-byte cells, 16-byte aligned "
+                        "bases, ld*size and stride*size, and rows, cols multiples of 16/size");
+        return run_vtiled(a);
     }
     if (k == DESC_KERNEL_SMEM) return run_smem(a);
     if (k == DESC_KERNEL_TILED || (k == DESC_KERNEL_AUTO && (!tma_ok || tiled_preferred(a))))

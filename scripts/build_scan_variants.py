@@ -14,6 +14,7 @@ VARIANTS = {
 }
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)
-with ThreadPoolExecutor(len(VARIANTS)) as ex:
-    for name, p in zip(VARIANTS, ex.map(lambda kv: B.build(defines=kv[1], out=os.path.join(out_dir, f"lib_{kv[0]}.so")), VARIANTS.items())):
+names = sys.argv[1:] or list(VARIANTS)
+with ThreadPoolExecutor(8) as ex:
+    for name, p in zip(names, ex.map(lambda n: B.build(defines=VARIANTS[n], out=os.path.join(out_dir, f"lib_{n}.so")), names)):
         print(name, p)

@@ -1,16 +1,36 @@
-"""Compile-time variants of the TILED transpose kernel for A/B runs (DESC_LIB=<path>)."""
+"""Compile-time variants of the TILED transpose kernel for A/B runs (DESC_LIB=<path>).
+
+  python scripts/build_tiled_variants.py [name ...]     (default: every variant below)
+"""
 import os, sys
 from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2305_03448_b200 import build as B
 
 VARIANTS = {
+    # r02 tile-shape sweep (8-byte cells)
     "s1": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=64"],
     "s2": ["DESC_TILED_TR8=64", "DESC_TILED_TC8=32"],
     "s3": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=32"],
+    # r03: cp.async staging, banded raster orders, cache hints, occupancy
+    "cpa5": ["DESC_TILED_CPA=1"],
+    "cpa8": ["DESC_TILED_CPA=1", "DESC_TILED_MINB=8"],
+    "r4": ["DESC_TILED_RASTER=4"],
+    "r8": ["DESC_TILED_RASTER=8"],
+    "r16": ["DESC_TILED_RASTER=16"],
+    "r32": ["DESC_TILED_RASTER=32"],
+    "ldcs": ["DESC_TILED_LD=1"],
+    "ldlu": ["DESC_TILED_LD=3"],
+    "stcs": ["DESC_TILED_ST=1"],
+    "stcg": ["DESC_TILED_ST=2"],
+    "ldcs_stcs": ["DESC_TILED_LD=1", "DESC_TILED_ST=1"],
+    "minb6": ["DESC_TILED_MINB=6"],
+    # r02 (session 2): the 16-byte vector tile kernel without cp.async (LDG.128 -> STS.128)
+    "vt_nocpa": ["DESC_VT_CPA=0"],
 }
+names = sys.argv[1:] or [n for n in VARIANTS if n not in ("s1", "s2", "s3")]
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)
-with ThreadPoolExecutor(len(VARIANTS)) as ex:
-    for name, p in zip(VARIANTS, ex.map(lambda kv: B.build(defines=kv[1], out=os.path.join(out_dir, f"lib_tiled_{kv[0]}.so")), VARIANTS.items())):
+with ThreadPoolExecutor(8) as ex:
+    for name, p in zip(names, ex.map(lambda n: B.build(defines=VARIANTS[n], out=os.path.join(out_dir, f"lib_tiled_{n}.so")), names)):
         print(name, p)

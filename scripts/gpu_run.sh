@@ -10,7 +10,8 @@
 #   dist1      configs[4] on one GPU: 65536^2 f32, every element verified
 #   gloo2      the N > 1 code path with 2 ranks sharing the GPU (gloo, host-staged
 #              all-to-all, peer path through CUDA IPC), 16384^2
-#   sanitize   product sanitizer gates + positive controls (scripts/gpu_sanitize.sh)
+#   sanitize   product sanitizer gates + positive controls (scripts/gpu_sanitize.sh; the
+#              pool has refused compute-sanitizer since r02 session 2 -> exits 3, SKIPPED)
 #   launches   ncu launch list (gpu__time_duration) of the default bench command
 #   ncu:<w>:<kernel regex>   one ncu --set full capture of that kernel in that workload
 #   exp:<script args>        python scripts/<script> <args>

@@ -19,7 +19,7 @@ import paper_2305_03448_b200 as desc  # noqa: E402
 
 CASES = [  # (batch, rows, cols, es)
     (1, 64, 64, 8), (1, 67, 131, 4), (1, 131, 67, 8), (1, 300, 500, 4), (3, 33, 65, 4),
-    (2, 130, 70, 8), (1, 5, 3, 4), (1, 256, 512, 2), (1, 257, 300, 1),
+    (2, 130, 70, 8), (1, 5, 3, 4), (1, 256, 512, 2), (1, 257, 300, 1), (1, 68, 132, 4),
 ]
 DT = {1: "u8", 2: "f16", 4: "f32", 8: "f64"}
 TI = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
@@ -38,6 +38,8 @@ def main():
         xin[:, :, :cols] = torch.from_numpy(src.view(NI[es])).cuda()
         ref = oracle.transpose(src)
         kernels = ["smem", "tiled", "tma"] + (["tma_st", "tma_tile"] if es in (4, 8) and rows * es >= 16 else [])
+        if es in (4, 8) and rows % v == 0 and cols % v == 0:
+            kernels.append("vtiled")      # 16-byte cp.async staging (rows, cols multiples of 16/es)
         for k in kernels:
             out = torch.zeros((batch, cols, ld_out), dtype=TI[es], device="cuda")
             desc.desc_transpose_ex(xin.data_ptr(), out.data_ptr(), batch, rows, cols, ld_in,

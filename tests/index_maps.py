@@ -172,6 +172,73 @@ def tiled_launch(batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, mu
     return L
 
 
+# ------------------------------------------------------------------ VTILED (16-byte vectors)
+def vtiled_launch(batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, TCH=None, NT=None,
+                  mutant=None, swizzle=True):
+    """csrc/vtiled_transpose.cuh transpose_vtiled_kernel restated at element granularity.
+    Tile TR = 16 VEC rows x TCH 16-byte chunks (VEC = 16 / es cells each), one NT-thread CTA
+    per tile (desc_transpose.cu run_vtiled defaults: 64 x 64 cells / 128 threads for 4-byte
+    cells, 32 x 32 / 64 for 8-byte).  Copy-in: chunk q = tid + NT k -> row q / TCH, chunk
+    q % TCH, stored at chunk (q % TCH) ^ ((row / VEC) & 7); copy-out: micro-block b = tid +
+    NT m -> (mr, mc) = (b % 16, b / 16), VEC 16-byte reads of rows VEC mr + k at chunk
+    mc ^ (mr & 7), output row VEC mc + j gets cells x[k][j].  mutant in {None, "tile_only"
+    (12: o = x[j], untransposed), "no_sync" (14)}; swizzle=False drops the XOR (a teeth check
+    for the conflict counter); requires rows, cols multiples of VEC."""
+    sw = 1 if swizzle else 0
+    VEC = 16 // es
+    if TCH is None:
+        TCH, NT = (16, 64) if es == 8 else (16, 128)
+    TR, TC = 16 * VEC, TCH * VEC
+    assert rows % VEC == 0 and cols % VEC == 0
+    tiles_r, tiles_c = -(-rows // TR), -(-cols // TC)
+    L = Launch()
+    tid = np.arange(NT)
+    e = np.arange(VEC)
+    for t in range(tiles_r * tiles_c * batch):
+        bt, rem = divmod(t, tiles_r * tiles_c)
+        ti, tj = divmod(rem, tiles_c)
+        r0, c0 = ti * TR, tj * TC
+        full = r0 + TR <= rows and c0 + TC <= cols
+        nr, nc = min(rows - r0, TR), min(cols - c0, TC)
+        tile = np.full(TR * TCH * VEC, UNWRITTEN, dtype=np.int64)
+        for k in range(TR * TCH // NT):                                    # copy-in
+            q = tid + NT * k
+            w, c = q // TCH, q % TCH
+            mk = np.ones(NT, bool) if full else (w < nr) & (c * VEC < nc)
+            phys = w * TCH + (c ^ (sw * ((w // VEC) & 7)))
+            for p in range(NT // 8):                                       # 8-lane phases
+                sel = slice(8 * p, 8 * p + 8)
+                if mk[sel].all() and np.unique(phys[sel] & 7).size != 8:
+                    L.bank_conflicts += 1
+            cells = phys[mk][:, None] * VEC + e[None, :]
+            src = bt * stride_in + (r0 + w[mk])[:, None] * ld_in + c0 + (c[mk] * VEC)[:, None] + e[None, :]
+            tile[cells] = src
+            L.sm((t, 0), np.broadcast_to(tid[mk][:, None], cells.shape), cells, True)
+        iv = 0 if mutant == "no_sync" else 1
+        for m in range(16 * TCH // NT):                                    # copy-out
+            b = tid + NT * m
+            mr, mc = b & 15, b >> 4
+            mk = np.ones(NT, bool) if full else (VEC * mr < nr) & (VEC * mc < nc)
+            x = np.zeros((NT, VEC, VEC), dtype=np.int64)                   # [thread][k][cell]
+            for k in range(VEC):
+                phys = (VEC * mr + k) * TCH + (mc ^ (sw * (mr & 7)))
+                for p in range(NT // 8):
+                    sel = slice(8 * p, 8 * p + 8)
+                    if mk[sel].all() and np.unique(phys[sel] & 7).size != 8:
+                        L.bank_conflicts += 1
+                cells = phys[:, None] * VEC + e[None, :]
+                x[:, k, :] = tile[cells]
+                L.unwritten_reads += int((x[mk, k, :] == UNWRITTEN).sum())
+                L.sm((t, iv), np.broadcast_to(tid[mk][:, None], cells[mk].shape), cells[mk], False)
+            for j in range(VEC):
+                mj = mk & ((VEC * mc + j < nc) | full)
+                o = x[:, j, :] if mutant == "tile_only" else x[:, :, j]    # o[k] = x[k][j]
+                dst = (bt * stride_out + (c0 + VEC * mc + j)[:, None] * ld_out + r0
+                       + (VEC * mr)[:, None] + e[None, :])
+                L.write(dst[mj], o[mj])
+    return L
+
+
 # ------------------------------------------------------------------ SMEM (Listing 1 schedule)
 def smem_launch(batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, grid=None,
                 mutant=None):

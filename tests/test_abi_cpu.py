@@ -66,6 +66,20 @@ def test_sass_is_sm100a_with_tma(lib):
         assert "UTMASTG" in blk, "TMA-store kernel does not issue bulk tensor stores"
 
 
+def test_sass_vtiled_is_16_byte_cp_async(lib):
+    """DESC_KERNEL_VTILED (csrc/vtiled_transpose.cuh): every global and shared access 16 bytes
+    wide -- cp.async.cg 16-byte copies (LDGSTS.E.BYPASS.128) into shared memory, LDS.128
+    micro-block reads, STG.E.128 stores; no 4-byte global access."""
+    out = subprocess.run(["cuobjdump", "-sass", desc.lib_path], capture_output=True, text=True,
+                         check=True).stdout
+    blocks = [b for b in out.split("Function : ")[1:] if "transpose_vtiled_kernel" in b[:200]]
+    assert len(blocks) >= 2, "vector tile kernels missing from the cubin"
+    for blk in blocks:
+        assert "LDGSTS.E.BYPASS.128" in blk and "LDGDEPBAR" in blk
+        assert "LDS.128" in blk and "STG.E.128" in blk
+        assert "STG.E " not in blk and "LDG.E " not in blk
+
+
 def test_product_build_carries_no_test_defects(lib):
     """The test-teeth defects (csrc/mutants.cuh) exist only in the -DDESC_MUTANTS variant."""
     with open(desc.lib_path, "rb") as f:

@@ -100,6 +100,41 @@ def test_tma_load_map_is_a_race_free_bijection(es):
         assert _check(L, shape) == [], shape
 
 
+def _vtiled_shapes(es):
+    """The vector tile kernel's rules: 16-byte pitches and rows, cols multiples of 16/es."""
+    v = 16 // es
+    out = []
+    for (b, r, c, *_) in SHAPES + [(1, 132, 68, 0, 0, 0, 0), (2, 96, 200, 0, 0, 0, 0)]:
+        r, c = -(-r // v) * v, -(-c // v) * v
+        li, lo = c + (v if b > 1 else 0), r + v
+        out.append((b, r, c, li, lo, r * li + v if b > 1 else 0, c * lo + 2 * v if b > 1 else 0))
+    return out
+
+
+@pytest.mark.parametrize("es", [4, 8])
+def test_vtiled_map_is_a_race_free_conflict_free_bijection(es):
+    """transpose_vtiled_kernel (csrc/vtiled_transpose.cuh), default tile per cell size and the
+    DESC_VTILED_CFG alternatives: every output element once with its transpose source, no
+    shared-memory race, every 8-lane phase of the 16-byte copy-in and copy-out conflict-free
+    (the 16-byte XOR swizzle)."""
+    cfgs = {4: [(16, 128), (16, 256), (32, 256), (8, 128), (16, 64), (32, 128), (8, 64)],
+            8: [(16, 64), (16, 256), (32, 256), (8, 128), (16, 128), (32, 128), (32, 64)]}
+    for shape in _vtiled_shapes(es):
+        for TCH, NT in cfgs[es]:
+            L = IM.vtiled_launch(*shape, es, TCH=TCH, NT=NT)
+            assert _check(L, shape) == [], (shape, TCH, NT)
+
+
+def test_vtiled_mutants_and_unswizzled_layout_rejected():
+    shape = (1, 100, 132, 132, 104, 0, 0)
+    for mutant, what in (("tile_only", "wrong source"), ("no_sync", "race")):
+        errs = _check(IM.vtiled_launch(*shape, 4, mutant=mutant), shape)
+        assert errs and any(what in e for e in errs), (mutant, errs)
+    for es in (4, 8):       # without the XOR swizzle the micro-block reads conflict
+        errs = _check(IM.vtiled_launch(*shape, es, swizzle=False), shape)
+        assert errs and all("bank conflict" in e for e in errs), errs
+
+
 # ------------------------------------------------------------------ teeth
 def test_tiled_mutants_rejected():
     shape = (1, 100, 131, 131, 100, 0, 0)        # edge tiles in both directions
