@@ -150,10 +150,12 @@ desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
 
 /* Host-buffer transpose (same operation and layout rules as desc_transpose_batched,
  * but h_in / h_out are HOST memory -- pinned for full PCIe overlap, pageable works).
- * The library streams row bands of the input through the caller-provided device
- * workspace d_work (256-byte aligned, work_bytes >= desc_transpose_host_workspace
- * recommended; smaller works down to one row): H2D copy of band k+1, transpose of
- * band k and D2H copy of band k-1 overlap on two internal streams.  When that would
+ * The library streams column bands of the input (= row bands of the output: 2-D H2D
+ * copies, contiguous D2H copies -- PCIe reads strided host rows faster than it writes
+ * them) through the caller-provided device workspace d_work (256-byte aligned,
+ * work_bytes >= desc_transpose_host_workspace recommended; smaller works down to one
+ * column): H2D copy of band k+1, transpose of band k and D2H copy of band k-1 overlap on
+ * two internal streams.  When that would
  * take more than 64 bands (e.g. many small batched matrices) and both host buffers are
  * page-locked and mapped, one TILED kernel instead reads and writes the host buffers
  * directly over PCIe (zero-copy; d_work is then unused).  Asynchronous on
@@ -301,7 +303,8 @@ desc_status desc_slab_transpose_peer(const void *in_slab, void *const *out_slabs
 desc_status desc_read_probe(const void *in, size_t bytes, void *sink, void *stream);
 size_t desc_read_probe_sink_bytes(void);
 
-/* Recommended workspace bytes for desc_transpose_host (double-buffered 512-row bands). */
+/* Recommended workspace bytes for desc_transpose_host (double-buffered 1024-column bands,
+ * or 512-row bands if larger). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);
 
 /* Number of kernel launches the last successful call of this thread issued (0 for an

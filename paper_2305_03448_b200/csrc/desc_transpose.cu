@@ -1064,13 +1064,22 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     if ((reinterpret_cast<uintptr_t>(d_work) & 255) != 0)
         return fail(DESC_ERR_SHAPE, "d_work must be 256-byte aligned");
 
-    // largest band (multiple of 128 rows when possible) whose double buffers fit d_work
-    int64_t band = rows;
-    while (band > 1 && band_bytes(band, cols, es) > (int64_t)work_bytes)
+    // Band axis.  Input-row bands make every H2D copy contiguous and every D2H copy 2-D
+    // (cols rows of band*size bytes); bands of input COLUMNS (= output rows) make the H2D
+    // 2-D and the D2H contiguous.  PCIe Gen5 on B200 reads strided host rows faster than it
+    // writes them (scripts/exp_pcie2d.py, profiles/r02_exp_pcie2d.txt, both directions
+    // concurrent, 8192^2 f32: 2-KB strided rows 86.2 vs 81.1 GB/s, 4-KB 89.6 vs 86.1), so
+    // AUTO bands by columns.  DESC_HOST_AXIS=1 forces row bands, =2 column bands (A/B).
+    static const int host_axis = dev_knob("DESC_HOST_AXIS", 0);
+    const bool by_cols = host_axis != 1;
+    const int64_t span = by_cols ? cols : rows, other = by_cols ? rows : cols;
+    // largest band (multiple of 128 when possible) whose double buffers fit d_work
+    int64_t band = span;
+    while (band > 1 && band_bytes(band, other, es) > (int64_t)work_bytes)
         band = band > 256 ? (band / 2 + 127) / 128 * 128 : band / 2;
-    if (band_bytes(band, cols, es) > (int64_t)work_bytes)
+    if (band_bytes(band, other, es) > (int64_t)work_bytes)
         return fail(DESC_ERR_SHAPE, "d_work (%zu bytes) too small: need >= %lld", work_bytes,
-                    (long long)band_bytes(1, cols, es));
+                    (long long)band_bytes(1, other, es));
 
     // Zero-copy mode: when both host buffers are page-locked and mapped, the TILED kernel
     // reads the input and writes the transposed output straight over PCIe in one pass.
@@ -1080,7 +1089,7 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     // would be cut into many small copies (> 64 bands, e.g. 256 x 1024^2: 62 GB/s banded vs
     // 75 GB/s zero-copy).  DESC_HOST_MODE=1 forces bands, =2 forces zero-copy (A/B).
     static const int host_mode = dev_knob("DESC_HOST_MODE", 0);
-    const int64_t nbands = batch * ((rows + band - 1) / band);
+    const int64_t nbands = batch * ((span + band - 1) / band);
     void *dz_in = nullptr, *dz_out = nullptr;
     if ((host_mode == 2 || (host_mode == 0 && nbands > 64)) && mapped_host(h_in, &dz_in) &&
         mapped_host(h_out, &dz_out)) {
@@ -1093,9 +1102,11 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     HostPipe *hp;
     if (desc_status s = host_pipe(dev, &hp)) return s;
     const int64_t v = 16 / es;
-    const int64_t ldi_d = round_up(cols, v);
-    const int64_t in_b = round_up(band * ldi_d * es, 256);
-    const int64_t out_b = round_up(cols * round_up(band, v) * es, 256);
+    // row bands: band x cols in, cols x band out; column bands: rows x band in, band x rows
+    // out (each 16-byte padded; the two together are what band_bytes counts)
+    const int64_t wide = round_up(band * round_up(other, v) * es, 256);
+    const int64_t narrow = round_up(other * round_up(band, v) * es, 256);
+    const int64_t in_b = by_cols ? narrow : wide, out_b = by_cols ? wide : narrow;
     char *w = static_cast<char *>(d_work);
     char *d_in[2] = {w, w + in_b};
     char *d_out[2] = {w + 2 * in_b, w + 2 * in_b + out_b};
@@ -1107,22 +1118,26 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     int launches = 0;
     int64_t k = 0;
     for (int64_t b = 0; b < batch; ++b) {
-        for (int64_t r0 = 0; r0 < rows; r0 += band, ++k) {
+        for (int64_t p0 = 0; p0 < span; p0 += band, ++k) {
             // fixed bands: measured 81 GB/s vs 77 GB/s with bands ramped at both ends
-            // (scripts/exp_e2e_ramp.py; narrow bands make strided D2H rows short)
-            const int64_t nr = rows - r0 < band ? rows - r0 : band;
+            // (scripts/exp_e2e_ramp.py; narrow bands make the strided rows short)
+            const int64_t np_ = span - p0 < band ? span - p0 : band;
             const int buf = (int)(k & 1);
             cudaStream_t s = hp->s[buf];
-            const int64_t ldo_d = round_up(nr, v);
-            const char *src = static_cast<const char *>(h_in) + (b * stride_in + r0 * ld_in) * es;
-            e = cudaMemcpy2DAsync(d_in[buf], ldi_d * es, src, ld_in * es, cols * es, nr,
+            // this band's sub-matrix: nr x nc input cells at (r0, c0)
+            const int64_t r0 = by_cols ? 0 : p0, c0 = by_cols ? p0 : 0;
+            const int64_t nr = by_cols ? rows : np_, nc = by_cols ? np_ : cols;
+            const int64_t ldi_d = round_up(nc, v), ldo_d = round_up(nr, v);
+            const char *src = static_cast<const char *>(h_in) + (b * stride_in + r0 * ld_in + c0) * es;
+            e = cudaMemcpy2DAsync(d_in[buf], ldi_d * es, src, ld_in * es, nc * es, nr,
                                   cudaMemcpyHostToDevice, s);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync H2D");
-            Args a{d_in[buf], d_out[buf], 1, nr, cols, ldi_d, ldo_d, 0, 0, es, s};
+            Args a{d_in[buf], d_out[buf], 1, nr, nc, ldi_d, ldo_d, 0, 0, es, s};
             if (desc_status st = dispatch(a, DESC_KERNEL_AUTO)) return st;
             ++launches;
-            char *dst = static_cast<char *>(h_out) + (b * stride_out + r0) * es;
-            e = cudaMemcpy2DAsync(dst, ld_out * es, d_out[buf], ldo_d * es, nr * es, cols,
+            // output block: rows c0 .. c0 + nc, columns r0 .. r0 + nr
+            char *dst = static_cast<char *>(h_out) + (b * stride_out + c0 * ld_out + r0) * es;
+            e = cudaMemcpy2DAsync(dst, ld_out * es, d_out[buf], ldo_d * es, nr * es, nc,
                                   cudaMemcpyDeviceToHost, s);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync D2H");
         }
@@ -1898,10 +1913,13 @@ desc_status desc_transpose_host(const void *h_in, void *h_out, int64_t batch, in
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype) {
     const int es = dtype_size(dtype);
     if (es == 0 || rows <= 0 || cols <= 0) return 0;
-    // 512-row bands: measured best trade-off between pipeline fill/drain and per-copy DMA
-    // efficiency on PCIe Gen5 (scripts/exp_e2e.py: 256 -> 72.7, 512 -> 82.9, 1024 -> 78.9 GB/s)
-    const int64_t band = rows < 512 ? rows : 512;
-    return (size_t)band_bytes(band, cols, es);
+    // Bands: the trade-off between pipeline fill/drain and per-copy DMA efficiency on PCIe
+    // Gen5, 8192^2 f32 (scripts/exp_e2e.py): column bands (AUTO) 256 -> 85.7, 512 -> 87.3,
+    // 1024 -> 88.0, 2048 -> 87.7 GB/s; row bands 256 -> 71.8, 512 -> 82.5, 1024 -> 82.5
+    // (profiles/r02_exp_e2e_axis.txt).  Sized for either axis (run_host, DESC_HOST_AXIS).
+    const int64_t br = rows < 512 ? rows : 512, bc = cols < 1024 ? cols : 1024;
+    const int64_t a = band_bytes(br, cols, es), b = band_bytes(bc, rows, es);
+    return (size_t)(a > b ? a : b);
 }
 
 desc_status desc_ipc_handle(const void *dptr, void *handle_out, uint64_t *offset_out) {

@@ -100,6 +100,9 @@ CHECKS = {
     "tiled_padded_f64": lambda: padded("tiled", 130, 197, 8, 199, 131),
     "tiled_described_f32": lambda: described("tiled", 2048, 2048, 4, reps=3),
     "tiled_random_f64": lambda: tight("tiled", 1000, 1500, 8, 12, specials=True, reps=3),
+    "vtiled_padded_f32": lambda: padded("vtiled", 68, 132, 4, 136, 72),
+    "vtiled_described_f32": lambda: described("vtiled", 2048, 2048, 4, reps=3),
+    "vtiled_random_f64": lambda: tight("vtiled", 1000, 1500, 8, 12, specials=True, reps=3),
     "scan_stream_i32": lambda: scan(1 << 22, "stream"),
     "scan_lookback_i32": lambda: scan(100003, "lookback"),
     "scan_three_pass_i32": lambda: scan(1 << 21, "three_pass"),

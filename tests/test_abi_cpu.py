@@ -145,7 +145,8 @@ def test_host_entry_validation(lib):
     assert _status(f, *args, 1, 8, 8, 8, 8, 0, 0, 42, FAKE_OUT, 4096, None) == 3    # dtype
     assert _status(f, h_in.ctypes.data, h_in.ctypes.data, 1, 8, 8, 8, 8, 0, 0, 0, FAKE_OUT,
                    4096, None) == 4                                                # alias
-    assert desc.desc_transpose_host_workspace(8192, 8192, "f32") == 2 * 2 * 512 * 8192 * 4
+    # double-buffered 1024-column bands (in: 8192 x 1024, out: 1024 x 8192), r02 band axis
+    assert desc.desc_transpose_host_workspace(8192, 8192, "f32") == 2 * 2 * 1024 * 8192 * 4
     assert desc.desc_transpose_host_workspace(0, 8, "f32") == 0
 
 

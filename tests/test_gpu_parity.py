@@ -4,6 +4,8 @@ Bit-exact is the only bar (R14: a transpose moves bits, no tolerance).
 Every kernel variant reachable by dispatch is run, plus each variant forced.  Outputs
 live inside guard bands and padded rows filled with a sentinel, which must survive.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -14,6 +16,7 @@ import paper_2305_03448_b200 as desc
 from paper_2305_03448_b200 import build as desc_build
 
 pytestmark = pytest.mark.gpu
+ROOT_DIR = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 GUARD = 4096  # bytes of sentinel before and after every output buffer
 SENT = 0xA5
@@ -412,6 +415,41 @@ def test_transpose_host_bands(pinned):
             assert desc.desc_last_launch_count() >= 1
             got = y.numpy().view(synth.UINT_OF_SIZE[es])
             assert got.tobytes() == oracle.transpose(src if batch > 1 else src[0]).tobytes()
+
+
+def test_transpose_host_both_band_axes():
+    """The host pipeline bands by input columns by default (strided H2D, contiguous D2H) and
+    by input rows with DESC_HOST_AXIS=1 (read once per process, hence the subprocess): both
+    bit-exact on ragged f32 / f64 shapes with padded pitches and a batch, many bands each."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+import oracle, synth, paper_2305_03448_b200 as desc
+for (batch, rows, cols, es, li, lo) in ((1, 1000, 777, 4, 780, 1003), (2, 333, 1024, 8, 1030, 340)):
+    src = synth.random_bits((batch, rows, cols), es, rows + cols)
+    ut = synth.UINT_OF_SIZE[es]
+    hin = torch.zeros((batch, rows, li), dtype=torch.int32 if es == 4 else torch.int64).pin_memory()
+    hin.numpy().view(ut)[:, :, :cols] = src
+    hout = torch.full((batch, cols, lo), -1, dtype=torch.int32 if es == 4 else torch.int64).pin_memory()
+    nbytes = desc.desc_transpose_host_workspace(64, 64, "f32" if es == 4 else "f64")
+    work = torch.empty(nbytes * 8, dtype=torch.uint8, device="cuda")
+    desc.desc_transpose_host(hin.data_ptr(), hout.data_ptr(), batch, rows, cols, li, lo,
+                             rows * li if batch > 1 else 0, cols * lo if batch > 1 else 0,
+                             "f32" if es == 4 else "f64", work.data_ptr(), work.numel())
+    torch.cuda.synchronize()
+    assert desc.desc_last_launch_count() > 2 * batch
+    got = hout.numpy().view(ut)
+    assert got[:, :, :rows].tobytes() == oracle.transpose(src).tobytes()
+    assert (hout.numpy()[:, :, rows:] == -1).all()
+print("ok")
+""" % ROOT_DIR
+    for axis in ("0", "1", "2"):
+        env = dict(os.environ, DESC_HOST_AXIS=axis)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert p.returncode == 0 and "ok" in p.stdout, (axis, p.stderr[-2000:])
 
 
 def test_transpose_host_zero_copy_many_bands():
