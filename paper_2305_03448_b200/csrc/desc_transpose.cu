@@ -1073,8 +1073,15 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     static const int host_axis = dev_knob("DESC_HOST_AXIS", 0);
     const bool by_cols = host_axis != 1;
     const int64_t span = by_cols ? cols : rows, other = by_cols ? rows : cols;
-    // largest band (multiple of 128 when possible) whose double buffers fit d_work
+    // largest band (multiple of 128 when possible) whose double buffers fit d_work, but
+    // at most span / DESC_HOST_BANDS (default 8, rounded up to 128): with fewer, larger
+    // bands the one-way fill (first H2D) and drain (last D2H) dominate small matrices
+    static const int min_bands = dev_knob("DESC_HOST_BANDS", 8);
     int64_t band = span;
+    if (min_bands > 1) {
+        const int64_t cap = round_up((span + min_bands - 1) / min_bands, 128);
+        if (cap < band) band = cap;
+    }
     while (band > 1 && band_bytes(band, other, es) > (int64_t)work_bytes)
         band = band > 256 ? (band / 2 + 127) / 128 * 128 : band / 2;
     if (band_bytes(band, other, es) > (int64_t)work_bytes)

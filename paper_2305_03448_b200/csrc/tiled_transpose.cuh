@@ -158,8 +158,15 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
     const int ox = tx % LPR, oy = tx / LPR;                 // copy-out lane split
     // this CTA's first tile (computed once: used by the prefetch and the first iteration)
     int64_t t = blockIdx.x;
+#if DESC_TILED_RASTER > 0
     int64_t bt, ti, tj;
     tiled_coords(t, tiles_r, tiles_c, bt, ti, tj);
+#else
+    const int64_t tiles_per_mat = tiles_r * tiles_c;
+    int64_t bt = t / tiles_per_mat;
+    int64_t ti = (t - bt * tiles_per_mat) / tiles_c;
+    int64_t tj = t - bt * tiles_per_mat - ti * tiles_c;
+#endif
 #if DESC_TILED_L2PF
     // While a previous grid may still run (PDL), warm L2 with this CTA's first input tile:
     // one prefetch per 128-byte line of its rows, no data to the SM, no ordering needed --
@@ -183,7 +190,15 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
     ptx::grid_dependency_wait();
     ptx::grid_launch_dependents();
     for (; t < ntiles; t += gridDim.x) {
-        if (t != (int64_t)blockIdx.x) tiled_coords(t, tiles_r, tiles_c, bt, ti, tj);
+        if (t != (int64_t)blockIdx.x) {
+#if DESC_TILED_RASTER > 0
+            tiled_coords(t, tiles_r, tiles_c, bt, ti, tj);
+#else
+            bt = t / tiles_per_mat;
+            ti = (t - bt * tiles_per_mat) / tiles_c;
+            tj = t - bt * tiles_per_mat - ti * tiles_c;
+#endif
+        }
         const int64_t r0 = ti * TR, c0 = tj * TC;
         const Cell *src = in + bt * stride_in + r0 * ld_in + c0;
         Cell *dst;
