@@ -256,9 +256,11 @@ desc_status desc_block_reduce(const void *in, void *out, int64_t n, int64_t bloc
  *   DESC_SCAN_LOOKBACK  : state reset + one launch, one 8-32 KB tile per CTA, decoupled look-back.
  *   DESC_SCAN_THREE_PASS: tile aggregates -> aggregate scan -> tile scans (3 launches,
  *                         3 n bytes of traffic; the paper's multi-kernel shape).
- *   DESC_SCAN_STREAM    : state reset + one launch, persistent CTAs stream 96 KB tiles through a
- *                         shared-memory ring (1-D TMA bulk copies) with a coalesced
- *                         look-back; 2 n bytes.  Needs 16-byte aligned in and out.
+ *   DESC_SCAN_STREAM    : state reset + one launch, persistent CTAs stream 32-48 KB tiles
+ *                         through a shared-memory ring (TMA loads) with a coalesced
+ *                         look-back; results of 4/8-byte types leave through swizzled
+ *                         staging and TMA tensor stores; 2 n bytes.  Needs 16-byte
+ *                         aligned in and out.
  * AUTO takes STREAM for aligned arrays of >= 2 tiles per SM, LOOKBACK for shorter ones,
  * THREE_PASS for unaligned long ones.  An explicit algorithm whose rule does not hold
  * gives DESC_ERR_KERNEL. */

@@ -1605,23 +1605,39 @@ int64_t scan_workspace_bytes(int64_t n, int es) {
 #ifndef DESC_SCAN_LB_WARPS
 #define DESC_SCAN_LB_WARPS 1
 #endif
+#ifndef DESC_SCAN_LC_F32       // f32: lane-contiguous layout + TMA-store staging
+#define DESC_SCAN_LC_F32 1
+#endif
+#ifndef DESC_SCAN_LC_I32       // 4-byte integers: same, NR warps per group
+#define DESC_SCAN_LC_I32 1
+#endif
+#ifndef DESC_SCAN_LC_I32_NR
+#define DESC_SCAN_LC_I32_NR 12
+#endif
+#ifndef DESC_SCAN_LC_F64       // 8-byte values: same
+#define DESC_SCAN_LC_F64 1
+#endif
 template <typename In> struct ScanPick {       // 4-byte integers
-    static constexpr int NR = 8, VPT = DESC_SCAN_VPT, S = DESC_SCAN_STAGES,
-                         QT = DESC_SCAN_TMEM_SLOTS;
+    static constexpr int NR = DESC_SCAN_LC_I32 ? DESC_SCAN_LC_I32_NR : 8,
+                         VPT = DESC_SCAN_LC_I32 ? 8 : DESC_SCAN_VPT,
+                         S = DESC_SCAN_LC_I32 ? 3 : DESC_SCAN_STAGES,
+                         QT = DESC_SCAN_TMEM_SLOTS, LC = DESC_SCAN_LC_I32;
 };
 template <> struct ScanPick<uint8_t> {         // 6 vectors per lane (16 elements each), 8 stages
-    static constexpr int NR = 8, VPT = 6, S = 8, QT = DESC_SCAN_TMEM_SLOTS;
+    static constexpr int NR = 8, VPT = 6, S = 8, QT = DESC_SCAN_TMEM_SLOTS, LC = 0;
 };
-template <> struct ScanPick<float> {
-    static constexpr int NR = 12, VPT = 8, S = 4, QT = 5;
+template <> struct ScanPick<float> {           // LC: 48 KB of store staging -> 3 stages
+    static constexpr int NR = 12, VPT = 8, S = DESC_SCAN_LC_F32 ? 3 : 4, QT = 5,
+                         LC = DESC_SCAN_LC_F32;
 };
 template <> struct ScanPick<double> {
-    static constexpr int NR = 12, VPT = 10, S = 3, QT = 4;
+    static constexpr int NR = 12, VPT = DESC_SCAN_LC_F64 ? 8 : 10, S = 3,
+                         QT = DESC_SCAN_LC_F64 ? 5 : 4, LC = DESC_SCAN_LC_F64;
 };
 template <> struct ScanPick<uint64_t> : ScanPick<double> {};
 template <typename In>
 using ScanStreamC = desc::ScanStreamCfg<ScanPick<In>::NR, ScanPick<In>::VPT, ScanPick<In>::S,
-                                        ScanPick<In>::QT, DESC_SCAN_LB_WARPS>;
+                                        ScanPick<In>::QT, DESC_SCAN_LB_WARPS, ScanPick<In>::LC>;
 
 // zero `bytes` (a multiple of 16) of scan state in stream order, PDL-chained
 desc_status scan_reset(char *work, int64_t bytes, const DevInfo &di, cudaStream_t stream) {
@@ -1674,7 +1690,7 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
     if (algo == DESC_SCAN_STREAM) {
         if (!vec) return fail(DESC_ERR_KERNEL, "streaming scan needs 16-byte aligned in and out");
         auto kern = desc::scan_stream_kernel<In, SP::NR, SP::VPT, SP::S, SP::QT,
-                                             DESC_SCAN_LB_WARPS>;
+                                             DESC_SCAN_LB_WARPS, SP::LC>;
         const int smem = SC::SMEM;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute (scan)");
@@ -1684,15 +1700,21 @@ desc_status launch_scan(const void *in, void *out, int64_t n, char *work, bool v
         const int64_t grid = ts < di.sms ? ts : di.sms;
         // TMA view of the input: rows of 128 bytes (the < 128-byte tail is read directly)
         const int64_t bulk_rows = n * es / 128;
-        CUtensorMap map;
+        CUtensorMap map, map_out;
         memset(&map, 0, sizeof(map));
+        memset(&map_out, 0, sizeof(map_out));
         if (bulk_rows > 0) {
             MapKey k{reinterpret_cast<uintptr_t>(in), 128 / es, bulk_rows, 1, 128 / es, 0, es,
                      128 / es, SC::BOX_ROWS};
             if (desc_status s = tensor_map(k, &map)) return s;
+            if (SP::LC) {     // the output as the same 128-byte rows, one warp segment per box
+                MapKey ko{reinterpret_cast<uintptr_t>(out), 128 / es, bulk_rows, 1, 128 / es, 0,
+                          es, 128 / es, 32};
+                if (desc_status s = tensor_map(ko, &map_out)) return s;
+            }
         }
-        e = launch_pdl(kern, (int)grid, SC::THREADS, smem, stream, map, pi, po, n, ts, bulk_rows,
-                       st);
+        e = launch_pdl(kern, (int)grid, SC::THREADS, smem, stream, map, map_out, pi, po, n, ts,
+                       bulk_rows, st);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "scan_stream launch");
         g_last_launches = 2;

@@ -19,8 +19,9 @@
 //    look-back: publish the aggregate (A), sum predecessors' A back to the nearest
 //    inclusive prefix (P), publish P, write the outputs.
 //  * THREE_PASS: tile aggregates -> one-CTA aggregate scan -> tile scans (3 n bytes).
-//  * STREAM: persistent CTAs stream 96 KB tiles through a shared-memory ring with 1-D TMA
-//    bulk copies, same look-back (2 n bytes).
+//  * STREAM: persistent CTAs stream 32-96 KB tiles through a shared-memory ring with TMA
+//    loads, same look-back (2 n bytes); 4- and 8-byte types use lane-contiguous tiles whose
+//    results leave through swizzled staging and TMA tensor stores (scan_stream_kernel, LC).
 // Tile descriptors are single-copy-atomic 64-bit {value, status} words: no fences (below).
 #pragma once
 #include <cstdint>
@@ -809,17 +810,24 @@ scan_tiles_kernel(const In *__restrict__ in, In *__restrict__ out, int64_t n,
 // warps run at most QT tiles ahead of the scan warps (TMEM slots) and S ring items ahead of
 // each other, so a slot is never rewritten while it is read.  Progress: tiles are claimed in
 // order by running CTAs and aggregates depend on nothing but their own bytes.
-template <int NR, int VPT, int S, int QT, int NLB>
+// LC = 1: lane-contiguous tile layout (lane owns VPT = 8 consecutive vectors, one 128-byte
+// row), the lane's exclusive prefix inside its warp parked in TMEM by the reduce warp (2
+// columns), the scan warps' results staged in a 128-byte-swizzled 4 KB buffer per warp and
+// written by one TMA tensor store (32 rows x 128 bytes) -- no shuffles in the scan warps and
+// fully coalesced stores.
+template <int NR, int VPT, int S, int QT, int NLB, int LC = 0>
 struct ScanStreamCfg {
     static constexpr int THREADS = 32 * (2 * NR + 2 + NLB);
     static constexpr int TB = NR * 32 * VPT * 16;      // tile bytes
     static constexpr int ROWS = TB / 128;              // 128-byte rows per tile (TMA view)
     static constexpr int NBOX = (ROWS + 255) / 256;    // boxes of <= 256 rows per tile
     static constexpr int BOX_ROWS = ROWS / NBOX;
-    static constexpr int SMEM = S * TB + 1024;         // stages 1024-byte aligned (swizzle)
+    static constexpr int WSEG = 32 * VPT * 16;         // bytes of one warp's segment
+    static constexpr int SMEM = S * TB + 1024 + (LC ? NR * WSEG : 0);   // + LC staging
+    static_assert(!LC || VPT == 8, "lane-contiguous layout: one 128-byte row per lane");
     static_assert(ROWS % NBOX == 0, "tile rows must split into equal TMA boxes");
     static constexpr int Q = QT + S + 2;               // tile metadata slots
-    static constexpr int WCOLS = 4 * VPT;              // TMEM columns per warp per tile
+    static constexpr int WCOLS = 4 * VPT + (LC ? 2 : 0);   // TMEM cols per warp per tile (+ LC prefix)
     static constexpr int TCOLS = (NR / 4) * WCOLS;     // TMEM columns per tile
 #ifndef DESC_SCAN_PASS
 #define DESC_SCAN_PASS 2          // scan warps: register passes per tile (A/B knob)
@@ -852,13 +860,14 @@ __device__ __forceinline__ uint64_t gtimer() {
 #define DESC_SCAN_DIAG 0      // 2 = outputs are the inputs (no scan arithmetic)
 #endif
 
-template <typename In, int NR, int VPT, int S, int QT, int NLB>
-__global__ void __launch_bounds__(ScanStreamCfg<NR, VPT, S, QT, NLB>::THREADS, 1)
-scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restrict__ in,
+template <typename In, int NR, int VPT, int S, int QT, int NLB, int LC = 0>
+__global__ void __launch_bounds__(ScanStreamCfg<NR, VPT, S, QT, NLB, LC>::THREADS, 1)
+scan_stream_kernel(const __grid_constant__ CUtensorMap map_in,
+                   const __grid_constant__ CUtensorMap map_out, const In *__restrict__ in,
                    In *__restrict__ out, int64_t n, int64_t ntiles, int64_t bulk_rows,
                    ScanState<typename AccOf<In>::T> st) {
     using Acc = typename AccOf<In>::T;
-    using C = ScanStreamCfg<NR, VPT, S, QT, NLB>;
+    using C = ScanStreamCfg<NR, VPT, S, QT, NLB, LC>;
     constexpr int V = 16 / sizeof(In);              // elements per 16-byte vector
     constexpr int TB = C::TB;
     constexpr int Q = C::Q;
@@ -1012,7 +1021,7 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
             const int qt = (int)(k % QT);
             ptx::mbar_wait(ptx::smem_u32(&full[s]), ph);
             const uint64_t tg = tag[s];
-            Acc wsum_v = 0;
+            Acc wsum_v = 0, lex = 0;
             uint4 x[VPT];
             if (tg != kScanSentinel) {
                 if (r == 0 && lane == 0) SCAN_TRACE(1, tg, gtimer());
@@ -1020,7 +1029,10 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                 const uint32_t sbase = ring + (uint32_t)s * TB;
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
-                    const int vi = (r * VPT + v) * 32 + lane;
+                    // round layout: vector v*32 + lane of the warp's segment; LC: vector
+                    // lane*VPT + v (row `lane` of the segment: under the 128-byte swizzle an
+                    // 8-lane phase reads 8 rows at 8 distinct chunks v ^ (lane & 7))
+                    const int vi = LC ? (r * 32 + lane) * VPT + v : (r * VPT + v) * 32 + lane;
                     const int64_t e0 = tbase + (int64_t)vi * V;
                     if (e0 + V <= n_bulk) {
                         const int w = vi >> 3;
@@ -1033,7 +1045,13 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                     }
                     wsum_v += vec_sum<In, Acc>(x[v]);
                 }
-                wsum_v = warp_sum(wsum_v);
+                if constexpr (LC) {   // lanes' exclusive prefixes go to the scan warps via TMEM
+                    const Acc incl = warp_incl_scan(wsum_v, lane);
+                    lex = warp_excl_from_incl(incl, lane);
+                    wsum_v = __shfl_sync(0xffffffffu, incl, 31);
+                } else {
+                    wsum_v = warp_sum(wsum_v);
+                }
             }
             // the warp total goes out before the TMEM slot is awaited: a tile's aggregate
             // depends on nothing but its bytes
@@ -1048,6 +1066,10 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                 const uint32_t tm = tmem_w + (uint32_t)(qt * C::TCOLS);
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) ptx::tmem_st4(tm + 4 * v, x[v]);
+                if constexpr (LC) {
+                    const uint64_t b = acc_bits(lex);
+                    ptx::tmem_st2(tm + 4 * VPT, (uint32_t)b, (uint32_t)(b >> 32));
+                }
                 ptx::tmem_wait_st();
                 ptx::tmem_fence_before_sync();
             }
@@ -1078,6 +1100,75 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
             ptx::mbar_wait(ptx::smem_u32(&parked[qt]), (uint32_t)(j / QT) & 1u);
             ptx::tmem_fence_after_sync();
             const uint32_t tm = tmem_w + (uint32_t)(qt * C::TCOLS);
+            if constexpr (LC) {
+                // lane-contiguous: start = tile prefix + warps before + the lane's exclusive
+                // prefix (parked by the reduce warp); vector sums, their running prefix, then
+                // each vector's elements from its own base; results into the swizzled staging
+                // row `lane`, one TMA tensor store of the warp's 4 KB segment
+                uint32_t plo, phi;
+                ptx::tmem_ld2(tm + 4 * VPT, plo, phi);
+                ptx::tmem_wait_ld();
+                asm volatile("" : "+r"(plo), "+r"(phi));
+                Acc run = rcarry + acc_from_bits<Acc>(((uint64_t)phi << 32) | plo);
+                const uint32_t stg = ring + (uint32_t)(S * TB + r * C::WSEG);
+                if (lane == 0) ptx::bulk_wait_group_read<0>();   // last store done reading
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < VPT; h += C::HALF) {
+                    constexpr int H = C::HALF;
+                    uint4 x[H];
+#pragma unroll
+                    for (int v = 0; v < H; ++v)
+                        if (h + v < VPT) x[v] = ptx::tmem_ld4(tm + 4 * (h + v));
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int v = 0; v < H; ++v)
+                        asm volatile("" : "+r"(x[v].x), "+r"(x[v].y), "+r"(x[v].z), "+r"(x[v].w));
+                    if (h + H >= VPT) {
+                        ptx::tmem_fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&freed[qt]));
+                    }
+                    Acc vb[H];
+#pragma unroll
+                    for (int v = 0; v < H; ++v) {
+                        vb[v] = run;
+                        if (h + v < VPT) run += vec_sum<In, Acc>(x[v]);
+                    }
+#pragma unroll
+                    for (int v = 0; v < H; ++v) {
+                        if (h + v >= VPT) break;
+                        const int vi = (r * 32 + lane) * VPT + h + v;
+                        const int64_t e0 = tbase + (int64_t)vi * V;
+                        uint4 o = make_uint4(0, 0, 0, 0);
+                        Acc ev = vb[v];
+#pragma unroll
+                        for (int e = 0; e < V; ++e) {
+                            ev += to_acc<Acc>(unpack<In>(x[v], e));
+                            set_elem<In>(o, e, (In)ev);
+                        }
+#if DESC_SCAN_DIAG & 2
+                        o = x[v];
+#endif
+                        if (e0 + V <= n_bulk) {
+                            ptx::sts128(stg + (uint32_t)(lane * 128 + (((h + v) ^ (lane & 7)) << 4)), o);
+                        } else {                     // tail beyond the TMA view
+#pragma unroll
+                            for (int e = 0; e < V; ++e)
+                                if (e0 + e < n) out[e0 + e] = unpack<In>(o, e);
+                        }
+                    }
+                }
+                ptx::fence_proxy_async_shared();     // staging writes -> async proxy
+                __syncwarp();
+                if (lane == 0) {
+                    const int64_t row0 = (tbase * (int64_t)sizeof(In) + (int64_t)r * C::WSEG) / 128;
+                    if (row0 < bulk_rows) {          // rows past the view are clipped by TMA
+                        ptx::tma_store_2d(&map_out, stg, 0, (int32_t)row0);
+                        ptx::bulk_commit_group();
+                    }
+                }
+            } else {
 #pragma unroll
             for (int h = 0; h < VPT; h += C::HALF) {
                 constexpr int H = C::HALF;
@@ -1129,7 +1220,11 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in, const In *__restr
                     }
                 }
             }
+            }   // round layout
         }
+    }
+    if constexpr (LC) {   // scan warps: their TMA stores have completed before the CTA exits
+        if (warp >= NR && warp < 2 * NR && lane == 0) ptx::bulk_wait_group<0>();
     }
     // release TMEM once both warp groups are done with it
     ptx::tmem_fence_before_sync();

@@ -11,6 +11,13 @@ VARIANTS = {
     "v16s3q4": ["DESC_SCAN_VPT=16", "DESC_SCAN_STAGES=3", "DESC_SCAN_TMEM_SLOTS=4"],
     "diag1": ["DESC_SCAN_DIAG=1"],
     "diag3": ["DESC_SCAN_DIAG=3"],
+    # r02 (session 2): f32 lane-contiguous layout with TMA-store staging
+    "lc": ["DESC_SCAN_LC_F32=1"],
+    "lc_diag1": ["DESC_SCAN_LC_F32=1", "DESC_SCAN_DIAG=1"],
+    "nolc": ["DESC_SCAN_LC_F32=0"],
+    "lc_i32": ["DESC_SCAN_LC_I32=1"],
+    "lc_i32_nr8": ["DESC_SCAN_LC_I32=1", "DESC_SCAN_LC_I32_NR=8"],
+    "lc_f64": ["DESC_SCAN_LC_F64=1"],
 }
 out_dir = os.path.join(B.ROOT, "build_variants")
 os.makedirs(out_dir, exist_ok=True)
