@@ -1397,15 +1397,25 @@ desc_status view_copy(const void *in, void *out, const desc_strided_view *view, 
     while ((1LL << vt.ulog) < w) ++vt.ulog;
     DevInfo di;
     if (desc_status st = device_info(dev, &di)) return st;
-    const int grid = (int)(vt.items < (int64_t)di.sms * 8 ? vt.items : (int64_t)di.sms * 8);
+    // Grid: mirrored 16-byte rows (mode 2) launch one work item per CTA and prefetch it into
+    // L2 before griddepcontrol.wait (rot180 8192^2 f32 0.955 -> 1.02); the other modes keep
+    // the persistent SMs x 8 grid (the tile view: one item per CTA 0.80, with the prefetch
+    // 0.64; profiles/r02_view_grid_pf.txt).  DESC_VIEW_GRID=0/1 and DESC_VIEW_PF=0/1 force
+    // either choice for every mode (A/B).
+    static const int view_grid = dev_knob("DESC_VIEW_GRID", -1);
+    static const int view_pf = dev_knob("DESC_VIEW_PF", -1);
+    const bool one = view_grid < 0 ? mode == 2 : view_grid == 1;
+    const int pf = view_pf < 0 ? (mode == 2 ? 1 : 0) : view_pf;
+    const int64_t cap = one ? ((int64_t)1 << 30) : (int64_t)di.sms * 8;
+    const int grid = (int)(vt.items < cap ? vt.items : cap);
     const char *ci = static_cast<const char *>(in);
     char *co = static_cast<char *>(out);
-    if (mode == 1) launch_plain_pdl(desc::view_tiles_kernel<uint4, 1>, grid, 256, 0, stream, ci, co, vt, es);
-    else if (mode == 2) launch_plain_pdl(desc::view_tiles_kernel<uint4, 2>, grid, 256, 0, stream, ci, co, vt, es);
-    else if (es == 8) launch_plain_pdl(desc::view_tiles_kernel<unsigned long long, 0>, grid, 256, 0, stream, ci, co, vt, es);
-    else if (es == 4) launch_plain_pdl(desc::view_tiles_kernel<uint32_t, 0>, grid, 256, 0, stream, ci, co, vt, es);
-    else if (es == 2) launch_plain_pdl(desc::view_tiles_kernel<uint16_t, 0>, grid, 256, 0, stream, ci, co, vt, es);
-    else launch_plain_pdl(desc::view_tiles_kernel<uint8_t, 0>, grid, 256, 0, stream, ci, co, vt, es);
+    if (mode == 1) launch_plain_pdl(desc::view_tiles_kernel<uint4, 1>, grid, 256, 0, stream, ci, co, vt, es, pf);
+    else if (mode == 2) launch_plain_pdl(desc::view_tiles_kernel<uint4, 2>, grid, 256, 0, stream, ci, co, vt, es, pf);
+    else if (es == 8) launch_plain_pdl(desc::view_tiles_kernel<unsigned long long, 0>, grid, 256, 0, stream, ci, co, vt, es, pf);
+    else if (es == 4) launch_plain_pdl(desc::view_tiles_kernel<uint32_t, 0>, grid, 256, 0, stream, ci, co, vt, es, pf);
+    else if (es == 2) launch_plain_pdl(desc::view_tiles_kernel<uint16_t, 0>, grid, 256, 0, stream, ci, co, vt, es, pf);
+    else launch_plain_pdl(desc::view_tiles_kernel<uint8_t, 0>, grid, 256, 0, stream, ci, co, vt, es, pf);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "view_tiles_kernel launch");
     g_last_launches = 1;

@@ -83,14 +83,38 @@ struct CellIO {
 // MODE 0: element cells (Cell), any s1.   MODE 1: 16-byte cells, s1 = +1.
 // MODE 2: 16-byte cells, s1 = -1 (mirrored load + in-register element reversal).
 // Short rows: up to 4 rows' loads are in flight per thread before their stores.
+// MODE 1 keeps 4 CTAs/SM (<= 64 registers) under its persistent grid: residency is what
+// keeps its loads in flight (74 registers = 3 CTAs/SM cost the tile view 0.95 -> 0.82).
 template <typename Cell, int MODE>
-__global__ void __launch_bounds__(256)
-view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const ViewTiles v, int es) {
-    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
-    ptx::grid_launch_dependents();
+__global__ void __launch_bounds__(256, MODE == 1 ? 4 : 0)
+view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const ViewTiles v, int es,
+                  int pf) {
     using IO = CellIO<Cell, MODE>;
     using T = typename IO::T;
     constexpr int CB = IO::CB;
+    if constexpr (MODE == 2) {
+        // mirrored rows (reverse views), launched one work item per CTA: L2 prefetch of the
+        // item's input rows, one per 128-byte line, before the dependency wait (as TILED,
+        // tiled_transpose.cuh: L2 is the point of coherence, a prefetch returns nothing to
+        // the SM and cannot fault) -- rot180 of 8192^2 f32 0.955 -> 1.02
+        if (pf && (int64_t)blockIdx.x < v.items) {
+            int64_t q = blockIdx.x;
+            const int64_t uc = q % v.n_uchunks; q /= v.n_uchunks;
+            const int64_t rc = q % v.n_rchunks; q /= v.n_rchunks;
+            const int64_t obase = outer_offset(v, q);
+            const int64_t r0 = rc * v.rch, nr = min(v.R2, r0 + v.rch) - r0;
+            const int64_t u0 = uc * v.uch, nu = min(v.U, u0 + v.uch) - u0;
+            const int64_t V = 16 / es, lpr = (nu * 16 + 127) / 128;     // lines per row
+            for (int64_t i = threadIdx.x; i < nr * lpr; i += blockDim.x) {
+                const int64_t rr = r0 + i / lpr, l = i % lpr;
+                // first input element of the row segment (walked backwards)
+                const int64_t e0 = obase + rr * v.s2 - (u0 + nu) * V + 1;
+                ptx::prefetch_l2(in + e0 * es + l * 128);
+            }
+        }
+    }
+    ptx::grid_dependency_wait();       // PDL: previous grid complete before any access
+    ptx::grid_launch_dependents();
     const int uw = 1 << v.ulog;                                    // thread cell width
     const int rpp = blockDim.x >> v.ulog;                          // rows per pass (>= 1)
     const int tu = threadIdx.x & (uw - 1);
