@@ -356,18 +356,19 @@ def test_config4_batched_256x1024sq_f32():
     assert y.cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(src).tobytes()
 
 
-def test_config5_65536_f32_every_element():
-    """65536 x 65536 f32 (16 GiB in + 16 GiB out, offsets beyond 2^31) in one AUTO launch,
-    hash-filled on device: ALL 2^32 output elements compared with the closed form
-    out[j][i] = H(i*N + j) (tests/fullcheck.py), plus 64 x 64 blocks at the corners and at
-    random places against the oracle itself."""
+@pytest.mark.parametrize("kernel", ["auto", "vtiled"])
+def test_config5_65536_f32_every_element(kernel):
+    """65536 x 65536 f32 (16 GiB in + 16 GiB out, offsets beyond 2^31) in one launch (AUTO,
+    and the 16-byte cp.async kernel), hash-filled on device: ALL 2^32 output elements
+    compared with the closed form out[j][i] = H(i*N + j) (tests/fullcheck.py), plus 64 x 64
+    blocks at the corners and at random places against the oracle itself."""
     from tests.fullcheck import hash_transpose_mismatches
     n = 65536
     seed = synth.BASE_SEED + 5
     x = torch.empty((n, n), dtype=torch.int32, device="cuda")
     synth.hash_fill_torch(x, 0, 0, n, seed, chunk_rows=2048)
     y = torch.empty_like(x)
-    desc.transpose(x.view(torch.float32), y.view(torch.float32))
+    desc.transpose(x.view(torch.float32), y.view(torch.float32), kernel=kernel)
     torch.cuda.synchronize()
     del x
     torch.cuda.empty_cache()
@@ -386,7 +387,7 @@ def test_config5_65536_f32_every_element():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("kernel", ["auto", "tma_st", "tma_tile"])
+@pytest.mark.parametrize("kernel", ["auto", "tma_st", "tma_tile", "vtiled"])
 def test_involution_full_size(kernel):
     """T6 at the BASELINE sizes: T(T(A)) == A bytewise for 8192^2 f32 and 3000 x 5000 f64."""
     for shape, es, dt in (((8192, 8192), 4, torch.float32), ((3000, 5000), 8, torch.float64)):
