@@ -452,6 +452,93 @@ def small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush, 
                                 "the 126 MB L2; context, not the metric)"}
 
 
+def live_ceiling_context(desc, torch, dev, stream, wl, xs, ys, R, batch, rows, cols, ld_in,
+                         step_bytes, kernel, graph: bool, reps: int = 20):
+    """Outside the timed region, on the same buffers and in the same launch pattern as the
+    metric (K launches back to back over the R rotating pairs): (1) the SAME BYTES moved by a
+    plain copy, no transpose -- this library's 16-byte row copy (desc_copy_batched, PDL) and
+    torch's copy_ -- the practical ceiling SURVEY 8(d) M3 asks to report beside the
+    transpose; (2) for small working sets, the transpose captured in a CUDA graph (2R
+    launches per graph) and replayed with events around each replay: the graph-captured
+    back-to-back median SURVEY 8(d) M2 asks for."""
+    import statistics as _st
+    sptr = stream.cuda_stream
+    tdt = xs[0].dtype
+
+    def region(fn, k=reps):
+        for i in range(3):
+            fn(i)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(k):
+            fn(i)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / k
+
+    def own_copy(i):
+        xi, yi = xs[i % R], ys[i % R]
+        desc.desc_copy_batched(xi.data_ptr(), yi.data_ptr(), batch, rows, cols, ld_in, cols,
+                               rows * ld_in, rows * cols, wl["dtype"], sptr)
+
+    def torch_copy(i):
+        xi, yi = xs[i % R], ys[i % R]
+        yi.view(batch, rows, cols).copy_(xi[..., :cols] if ld_in != cols else xi.view(batch, rows, cols))
+
+    out = {}
+    for name, fn in (("desc_copy_batched", own_copy), ("torch_copy", torch_copy)):
+        try:
+            ms = region(fn)
+            out[name + "_gbs"] = round(step_bytes / (ms / 1e3) / 1e9, 1)
+        except Exception as e:  # noqa: BLE001
+            out[name + "_error"] = f"{type(e).__name__}: {e}"[:200]
+    out["what"] = ("the same bytes (read + write) moved without transposing, same buffers, K "
+                   "launches back to back: the practical ceiling of this workload's layout")
+    if graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(stream)
+            n_in = 2 * R
+            with torch.cuda.stream(cs):
+                for i in range(n_in):        # warm the capture stream once
+                    xi, yi = xs[i % R], ys[i % R]
+                    desc.desc_transpose_ex(xi.data_ptr(), yi.data_ptr(), batch, rows, cols, ld_in,
+                                           rows, rows * ld_in if batch > 1 else 0,
+                                           rows * cols if batch > 1 else 0, wl["dtype"], kernel,
+                                           cs.cuda_stream)
+                torch.cuda.synchronize(dev)
+                with torch.cuda.graph(g, stream=cs):
+                    for i in range(n_in):
+                        xi, yi = xs[i % R], ys[i % R]
+                        desc.desc_transpose_ex(xi.data_ptr(), yi.data_ptr(), batch, rows, cols,
+                                               ld_in, rows, rows * ld_in if batch > 1 else 0,
+                                               rows * cols if batch > 1 else 0, wl["dtype"],
+                                               kernel, torch.cuda.current_stream(dev).cuda_stream)
+            stream.wait_stream(cs)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize(dev)
+            per = []
+            for _ in range(100):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                per.append(e0.elapsed_time(e1) / n_in)
+            med = _st.median(per)
+            out["graph_replay_ms_per_launch_median"] = round(med, 5)
+            out["graph_replay_gbs"] = round(step_bytes / (med / 1e3) / 1e9, 1)
+            out["graph_what"] = (f"{n_in} transposes over the {R} rotating pairs captured in one "
+                                 "CUDA graph (PDL edges kept), 100 replays with events around "
+                                 "each, median per launch")
+        except Exception as e:  # noqa: BLE001
+            out["graph_error"] = f"{type(e).__name__}: {e}"[:200]
+    return out
+
+
 def ours_arm(args, wl, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -595,6 +682,8 @@ def ours_arm(args, wl, world, rank, local):
     peak, peak_src = load_peak()
     small = small_problem_context(desc, torch, dev, stream, wl, kernel, step, l2_flush,
                                   step_bytes) if small_ws else None
+    ceiling = live_ceiling_context(desc, torch, dev, stream, wl, xs, ys, R, batch, rows, cols,
+                                   ld_in, step_bytes, kernel, graph=small_ws and not flush)
 
     # ---- parity of the timed output (rank-local) ------------------------------------
     parity = None
@@ -662,6 +751,7 @@ def ours_arm(args, wl, world, rank, local):
             "parity": parity,
             "gpu_launches": launches,
             **({"small_problem": small} if small else {}),
+            "same_bytes_copy": ceiling,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

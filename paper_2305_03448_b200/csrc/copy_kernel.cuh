@@ -6,8 +6,8 @@
 // identity view applied to a `group`-ed place (Listing 3) -- a copy between
 // two layouts of the same elements, no transposition.
 //
-// One CTA per row (grid-stride over batch*rows rows), threads stride over 16-byte (or
-// element-sized) units of the row, 4 units in flight per thread.
+// One CTA per row (a grid of batch*rows CTAs; grid-stride if capped), threads stride over
+// 16-byte (or element-sized) units of the row, UNR (4 or 8) units in flight per thread.
 #pragma once
 #include <cstdint>
 
@@ -15,7 +15,7 @@
 
 namespace desc {
 
-template <typename V>
+template <typename V, int UNR = 4>
 __global__ void __launch_bounds__(256)
 copy_rows_kernel(const char *__restrict__ in, char *__restrict__ out, int64_t rows,
                  int64_t total_rows, int64_t units, int64_t ld_in_b, int64_t ld_out_b,
@@ -39,13 +39,12 @@ copy_rows_kernel(const char *__restrict__ in, char *__restrict__ out, int64_t ro
         const V *src = reinterpret_cast<const V *>(in + b * stride_in_b + i * ld_in_b);
         V *dst = reinterpret_cast<V *>(out + b * stride_out_b + i * ld_out_b);
         int64_t u = threadIdx.x;
-        for (; u + 3 * blockDim.x < units; u += 4 * blockDim.x) {
-            const V v0 = src[u], v1 = src[u + blockDim.x], v2 = src[u + 2 * blockDim.x],
-                    v3 = src[u + 3 * blockDim.x];
-            dst[u] = v0;
-            dst[u + blockDim.x] = v1;
-            dst[u + 2 * blockDim.x] = v2;
-            dst[u + 3 * blockDim.x] = v3;
+        for (; u + (UNR - 1) * blockDim.x < units; u += UNR * blockDim.x) {
+            V v[UNR];
+#pragma unroll
+            for (int k = 0; k < UNR; ++k) v[k] = src[u + k * blockDim.x];
+#pragma unroll
+            for (int k = 0; k < UNR; ++k) dst[u + k * blockDim.x] = v[k];
         }
         for (; u < units; u += blockDim.x) dst[u] = src[u];
     }

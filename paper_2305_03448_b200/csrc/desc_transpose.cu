@@ -1187,14 +1187,30 @@ desc_status run_copy(const void *in, void *out, int64_t batch, int64_t rows, int
     DevInfo di;
     if (desc_status st = device_info(dev, &di)) return st;
     const int64_t total_rows = batch * rows;
-    const int grid = (int)(total_rows < (int64_t)di.sms * 8 ? total_rows : (int64_t)di.sms * 8);
+    // One row per CTA (the block scheduler balances the SMs and every CTA prefetches its row
+    // into L2 before the dependency wait, as TILED) and 8 16-byte loads in flight per thread
+    // when rows hold >= 8 per thread, else 4 (scripts/exp_copy.py,
+    // profiles/r02_copy_grid_unroll.txt, back to back: 8192^2 f32 0.962 -> 1.049, the slab
+    // unpack at P = 2 / 4 / 8 0.90 / 0.92 / 0.94 -> 1.009 / 1.041 / 1.039, 2048^2 f64 0.921 ->
+    // 0.981).  A/B knobs: DESC_COPY_GRID=0 the former persistent SMs x 8 grid, DESC_COPY_UNR=4/8.
+    static const int copy_grid = dev_knob("DESC_COPY_GRID", 1);
+    static const int copy_unr_knob = dev_knob("DESC_COPY_UNR", 0);
+    const int copy_unr = copy_unr_knob ? copy_unr_knob : (cols * es / 16 >= 8 * 256 ? 8 : 4);
+    // (short rows -- fewer than 256 16-byte units -- keep the persistent grid: a CTA per row
+    // would leave most of its threads idle)
+    const bool row_per_cta = copy_grid == 1 && cols * es >= 256 * 16;
+    const int64_t gcap = row_per_cta ? ((int64_t)1 << 30) : (int64_t)di.sms * 8;
+    const int grid = (int)(total_rows < gcap ? total_rows : gcap);
     const bool vec16 = (i0 % 16 == 0) && (o0 % 16 == 0) && (cols * es) % 16 == 0 &&
                        (ld_in * es) % 16 == 0 && (ld_out * es) % 16 == 0 &&
                        (batch == 1 || ((stride_in * es) % 16 == 0 && (stride_out * es) % 16 == 0));
     const char *ci = static_cast<const char *>(in);
     char *co = static_cast<char *>(out);
     const int64_t sib = batch > 1 ? stride_in * es : 0, sob = batch > 1 ? stride_out * es : 0;
-    if (vec16)
+    if (vec16 && copy_unr == 8)
+        launch_plain_pdl(desc::copy_rows_kernel<uint4, 8>, grid, 256, 0, stream, ci, co, rows, total_rows, cols * es / 16,
+                                                                  ld_in * es, ld_out * es, sib, sob);
+    else if (vec16)
         launch_plain_pdl(desc::copy_rows_kernel<uint4>, grid, 256, 0, stream, ci, co, rows, total_rows, cols * es / 16,
                                                                ld_in * es, ld_out * es, sib, sob);
     else if (es == 8)
