@@ -21,6 +21,10 @@
 //  12 TILED_TILE_ONLY    TILED kernel copies the tile out untransposed (Listing 2 literally)
 //  13 TILED_EDGE         TILED edge-tile store predicate off by one (one padding cell written)
 //  14 TILED_NO_SYNC      TILED kernel without the barrier between staging and copy-out (race)
+//  15 SCAN_LC_NO_SWIZZLE streaming scan writes its TMA-store staging linearly (the tensor map
+//                        unswizzles it: chunks land in the wrong places)
+//  16 SCAN_LC_NO_WAIT    streaming scan rewrites its staging without waiting for the previous
+//                        TMA store's reads and without the proxy fence (a race; may not manifest)
 #pragma once
 
 namespace desc {
@@ -41,6 +45,8 @@ enum DescMutant : int {
     MUT_TILED_TILE_ONLY = 12,
     MUT_TILED_EDGE = 13,
     MUT_TILED_NO_SYNC = 14,
+    MUT_SCAN_LC_NO_SWIZZLE = 15,
+    MUT_SCAN_LC_NO_WAIT = 16,
 };
 
 #ifdef DESC_MUTANTS

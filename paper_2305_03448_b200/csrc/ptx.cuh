@@ -196,6 +196,23 @@ __device__ __forceinline__ void fence_proxy_async_shared() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Consumer release of a TMA ring slot after reading it with ld.shared.  The next TMA load
+// into the slot is an async-proxy WRITE after these generic-proxy READS: the mbarrier
+// release/acquire pair orders the generic accesses only, so a proxy fence precedes the
+// arrive.  Without it the persistent TMA-load kernel (tma_transpose.cuh) produced wrong
+// elements in 1-2 of 300 launches of 8192^2 f32 (scripts/stress_8192.py; with the fence 0 of
+// 300; profiles/r02_tma_release_race.txt).  DESC_REL_MODE=0 drops the fence (A/B only).
+#ifndef DESC_REL_MODE
+#define DESC_REL_MODE 1
+#endif
+__device__ __forceinline__ void release_slot_after_lds(uint32_t bar, int lane) {
+#if DESC_REL_MODE == 1
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+}
+
 // Named barrier over `nthreads` threads (id 0 is __syncthreads).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -1111,7 +1111,8 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in,
                 asm volatile("" : "+r"(plo), "+r"(phi));
                 Acc run = rcarry + acc_from_bits<Acc>(((uint64_t)phi << 32) | plo);
                 const uint32_t stg = ring + (uint32_t)(S * TB + r * C::WSEG);
-                if (lane == 0) ptx::bulk_wait_group_read<0>();   // last store done reading
+                if (lane == 0 && !DESC_MUTANT(MUT_SCAN_LC_NO_WAIT))
+                    ptx::bulk_wait_group_read<0>();              // last store done reading
                 __syncwarp();
 #pragma unroll
                 for (int h = 0; h < VPT; h += C::HALF) {
@@ -1151,7 +1152,8 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in,
                         o = x[v];
 #endif
                         if (e0 + V <= n_bulk) {
-                            ptx::sts128(stg + (uint32_t)(lane * 128 + (((h + v) ^ (lane & 7)) << 4)), o);
+                            const int sw = DESC_MUTANT(MUT_SCAN_LC_NO_SWIZZLE) ? 0 : (lane & 7);
+                            ptx::sts128(stg + (uint32_t)(lane * 128 + (((h + v) ^ sw) << 4)), o);
                         } else {                     // tail beyond the TMA view
 #pragma unroll
                             for (int e = 0; e < V; ++e)
@@ -1159,7 +1161,8 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in,
                         }
                     }
                 }
-                ptx::fence_proxy_async_shared();     // staging writes -> async proxy
+                if (!DESC_MUTANT(MUT_SCAN_LC_NO_WAIT))
+                    ptx::fence_proxy_async_shared(); // staging writes -> async proxy
                 __syncwarp();
                 if (lane == 0) {
                     const int64_t row0 = (tbase * (int64_t)sizeof(In) + (int64_t)r * C::WSEG) / 128;

@@ -206,8 +206,8 @@ transpose_tma2_kernel(const __grid_constant__ CUtensorMap map_in,
                                       ((task_chunk(q) ^ sw) << 4));
             }
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty_bar[s]));   // release input slot
+        // release the slot: proxy fence (generic reads before the next TMA write), arrive
+        ptx::release_slot_after_lds(ptx::smem_u32(&empty_bar[s]), lane);
 
         // transposed micro-blocks -> output staging (swizzled like the output tensor map)
         const uint32_t obase = out_base + (it % OBUF) * C::OUT_BYTES;

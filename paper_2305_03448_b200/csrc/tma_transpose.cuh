@@ -289,8 +289,8 @@ transpose_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaParams p)
                                       ((task_chunk(q) ^ (row & 7)) << 4));
             }
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty_bar[s]));   // release slot
+        // release the slot: proxy fence (generic reads before the next TMA write), arrive
+        ptx::release_slot_after_lds(ptx::smem_u32(&empty_bar[s]), lane);
 
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {

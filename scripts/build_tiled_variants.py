@@ -27,6 +27,8 @@ VARIANTS = {
     "minb6": ["DESC_TILED_MINB=6"],
     # r02 (session 2): the 16-byte vector tile kernel without cp.async (LDG.128 -> STS.128)
     "vt_nocpa": ["DESC_VT_CPA=0"],
+    # TMA ring slot release after ld.shared without the proxy fence (ptx.cuh)
+    "rel0": ["DESC_REL_MODE=0"],
 }
 names = sys.argv[1:] or [n for n in VARIANTS if n not in ("s1", "s2", "s3")]
 out_dir = os.path.join(B.ROOT, "build_variants")

@@ -479,3 +479,27 @@ def test_transpose_host_rejects_device_buffers():
     with pytest.raises(desc.DescError, match="DESC_ERR_SHAPE"):
         desc.desc_transpose_host(h.data_ptr(), torch.empty_like(h).data_ptr(), 1, 64, 64, 64, 64,
                                  0, 0, "f32", work.data_ptr(), 16)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "tma", "tma_st", "tma_tile", "vtiled"])
+def test_repeated_launches_8192_no_intermittent_mismatch(kernel):
+    """Intermittent-race guard (r02): the persistent TMA-load kernel once released its ring
+    slot without a proxy fence between its ld.shared reads and the next TMA write -- 1-2 of
+    300 launches of 8192^2 f32 had wrong elements (profiles/r02_tma_release_race.txt).  300
+    launches per kernel, random and self-describing inputs, each output compared on the
+    device with the definition (torch's transposed view as the checker)."""
+    n = 8192
+    a = synth.random_bits((n, n), 4, synth.BASE_SEED + 2)
+    srcs = [torch.from_numpy(a.view(np.int32)).cuda(),
+            torch.arange(n * n, dtype=torch.int64, device="cuda").view(n, n).to(torch.int32)]
+    refs = [s.t().contiguous() for s in srcs]
+    y = torch.empty_like(srcs[0])
+    bad = []
+    for it in range(150):
+        for s, r in zip(srcs, refs):
+            y.fill_(-0x5A5A5A5B)
+            desc.transpose(s.view(torch.float32), y.view(torch.float32), kernel=kernel)
+            cnt = int((y != r).sum())
+            if cnt:
+                bad.append((it, cnt))
+    assert not bad, f"{kernel}: launches with mismatching elements (iteration, count): {bad[:5]}"

@@ -40,9 +40,11 @@ DETERMINISTIC = {
     11: ("REDUCE_NO_TAIL (scalar tail dropped)", ["reduce_i32"]),
     12: ("TILED_TILE_ONLY (tile copied out untransposed)", ["tiled_described_f32", "tiled_random_f64"]),
     13: ("TILED_EDGE (edge store predicate off by one)", ["tiled_padded_f32", "tiled_padded_f64"]),
+    15: ("SCAN_LC_NO_SWIZZLE (TMA-store staging written linearly)", ["scan_stream_i32"]),
 }
 RACE_ONLY = {9: "TMA2_NO_FENCE (proxy fence and WAR wait removed)",
-             14: "TILED_NO_SYNC (staging / copy-out barrier removed; TILED and VTILED)"}
+             14: "TILED_NO_SYNC (staging / copy-out barrier removed; TILED and VTILED)",
+             16: "SCAN_LC_NO_WAIT (staging rewritten before the TMA store read it; no proxy fence)"}
 # the TILED defects compiled into the 16-byte vector tile kernel too (csrc/vtiled_transpose.cuh):
 # a second family that must catch them independently
 ALSO = {12: ["vtiled_described_f32", "vtiled_random_f64"]}
