@@ -856,6 +856,10 @@ __device__ __forceinline__ uint64_t gtimer() {
 #define SCAN_TRACE(f, t, v) do { } while (0)
 #endif
 
+#ifndef DESC_SCAN_REL_FENCE   // proxy fence before a reduce warp releases its ring stage
+#define DESC_SCAN_REL_FENCE 1
+#endif
+
 #ifndef DESC_SCAN_DIAG        // diagnostics builds only (wrong results): 1 = no look-back,
 #define DESC_SCAN_DIAG 0      // 2 = outputs are the inputs (no scan arithmetic)
 #endif
@@ -1073,6 +1077,12 @@ scan_stream_kernel(const __grid_constant__ CUtensorMap map_in,
                 ptx::tmem_wait_st();
                 ptx::tmem_fence_before_sync();
             }
+#if DESC_SCAN_REL_FENCE
+            // the next TMA load into this stage is an async-proxy write after the ld.shared
+            // reads above (ptx.cuh release_slot_after_lds; here the reads have also been
+            // consumed -- sums, TMEM stores -- before the arrive)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
             __syncwarp();
             if (lane == 0) {
                 ptx::mbar_arrive(ptx::smem_u32(&empty[s]));             // stage reusable
