@@ -562,7 +562,7 @@ desc_status run_tma_tile(const Args &a) {
 // (16-byte bases, ld*size and stride*size multiples of 16) and rows, cols multiples of the
 // cells per 16-byte chunk, so edge tiles hold whole chunks and micro-blocks.
 bool vtiled_ok(const Args &a) {
-    if ((a.es != 4 && a.es != 8) || a.rev_rows || !tma_eligible(a)) return false;
+    if (a.rev_rows || !tma_eligible(a)) return false;
     const int64_t vec = 16 / a.es;
     return a.rows % vec == 0 && a.cols % vec == 0;
 }
@@ -613,8 +613,19 @@ desc_status run_vtiled(const Args &a) {
                 case 6: return launch_vtiled<8, 32, 64>(a);     // 32 x 64, 16 copies / thread
                 default: return launch_vtiled<8, 16, 64>(a);    // 32 x 32 cells, 8 KB
             }
+        case 2:
+            switch (cfg) {
+                case 1: return launch_vtiled<2, 16, 256>(a);    // 128 x 128, 8 copies / thread
+                case 2: return launch_vtiled<2, 8, 64>(a);      // 128 x 64, 16 copies / thread
+                default: return launch_vtiled<2, 8, 128>(a);    // 128 x 64 cells, 16 KB
+            }
+        case 1:
+            switch (cfg) {
+                case 1: return launch_vtiled<1, 8, 64>(a);      // 256 x 128, 32 copies / thread
+                default: return launch_vtiled<1, 8, 128>(a);    // 256 x 128 cells, 32 KB
+            }
     }
-    return fail(DESC_ERR_KERNEL, "vector tile kernel supports 4- and 8-byte elements only");
+    return fail(DESC_ERR_DTYPE, "unsupported element size %d", a.es);
 }
 
 template <typename Cell>
@@ -925,8 +936,8 @@ desc_status dispatch(const Args &a, desc_kernel k) {
     }
     if (k == DESC_KERNEL_VTILED) {
         if (!vtiled_ok(a))
-            return fail(DESC_ERR_KERNEL, "vector tile kernel needs 4/8-byte cells, 16-byte aligned "
-                        "bases, ld*size and stride*size, and rows, cols multiples of 16/size");
+            return fail(DESC_ERR_KERNEL, "vector tile kernel needs 16-byte aligned bases, ld*size "
+                        "and stride*size, and rows, cols multiples of 16/size");
         return run_vtiled(a);
     }
     if (k == DESC_KERNEL_SMEM) return run_smem(a);

@@ -11,20 +11,24 @@
 //     sits at chunk c ^ ((w / VEC) & 7) -- so the row-major copy-in (8 lanes of a phase:
 //     one row, 8 chunks) and the micro-block reads of the copy-out (8 lanes: 8 micro-rows,
 //     one chunk) both touch 8 distinct 16-byte bank groups: no conflicts, no padding,
-//   * each thread reads VEC x VEC micro-blocks (VEC = 16 / cell size: 4x4 f32, 2x2 f64) with
-//     VEC ld.shared.v4, transposes them in registers (pure renaming) and writes VEC 16-byte
-//     stores; 16 lanes cover one 256-byte output row segment, so every warp store
-//     instruction writes two fully coalesced 256-byte segments,
+//   * each thread reads VEC x VEC micro-blocks (VEC = 16 / cell size: 4x4 f32, 2x2 f64,
+//     8x8 16-bit, 16x16 bytes) with VEC ld.shared.v4, transposes them in registers (renaming
+//     for 4/8-byte cells, byte permutes for 1/2-byte cells) and writes VEC 16-byte stores;
+//     16 lanes cover one 256-byte output row segment, so every warp store instruction writes
+//     two fully coalesced 256-byte segments,
 //   * one tile per CTA in a 1-D grid, PDL with the L2 prefetch of the CTA's tile before
 //     griddepcontrol.wait (as TILED, tiled_transpose.cuh), predicated edge tiles.
-// Eligibility (host, vtiled_ok): 4/8-byte cells, 16-byte aligned bases, ld_in, ld_out (and
-// the batch strides) and rows, cols multiples of VEC -- edge tiles then hold whole chunks
-// and whole micro-blocks.
+// Eligibility (host, vtiled_ok): 16-byte aligned bases, ld_in, ld_out (and the batch
+// strides) and rows, cols multiples of VEC -- edge tiles then hold whole chunks and whole
+// micro-blocks.  Tile: TR = 16 VEC rows (64 f32, 32 f64, 128 16-bit, 256 bytes).
 #pragma once
 #include <cstdint>
 
+#include <utility>
+
 #include "mutants.cuh"
 #include "ptx.cuh"
+#include "tma_transpose.cuh"      // micro_row: the VEC x VEC register micro-transposes
 
 namespace desc {
 
@@ -41,7 +45,7 @@ namespace desc {
 template <int ES, int TCH_, int NT_>
 struct VTiledCfg {
     static constexpr int VEC = 16 / ES;                 // cells per 16-byte chunk
-    static constexpr int TR = 16 * VEC;                 // tile rows: 64 (4-byte), 32 (8-byte)
+    static constexpr int TR = 16 * VEC;                 // tile rows: 64 (4-byte), 32 (8-byte), ...
     static constexpr int TCH = TCH_;                    // chunks per tile row
     static constexpr int TC = TCH * VEC;                // tile cols (cells)
     static constexpr int NT = NT_;
@@ -51,10 +55,6 @@ struct VTiledCfg {
     static_assert(TCH >= 8 && (TCH & (TCH - 1)) == 0, "swizzle spans 8 chunks");
     static_assert(LPT * NT == TR * TCH && MPT * NT == 16 * TCH && MPT >= 1, "thread shape");
 };
-
-__device__ __forceinline__ uint32_t vt_word(const uint4 &v, int w) {
-    return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
-}
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -69,6 +69,22 @@ __device__ __forceinline__ uint4 ldg128(const void *p) {
     asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
+}
+
+template <int ES, int J>
+__device__ __forceinline__ void vt_emit_row(const uint4 (&x)[16 / ES], char *drow, int64_t ld_b,
+                                            int jmax) {
+    if (J < jmax) {
+        uint4 o = micro_row<ES, J>(x);
+        if (DESC_MUTANT(MUT_TILED_TILE_ONLY)) o = x[J];
+        ptx::stg128(drow + (int64_t)J * ld_b, o);
+    }
+}
+
+template <int ES, int... J>
+__device__ __forceinline__ void vt_emit(const uint4 (&x)[16 / ES], char *drow, int64_t ld_b,
+                                        int jmax, std::integer_sequence<int, J...>) {
+    (vt_emit_row<ES, J>(x, drow, ld_b, jmax), ...);
 }
 
 template <int ES, int TCH_, int NT_>
@@ -145,20 +161,11 @@ transpose_vtiled_kernel(const char *__restrict__ in, char *__restrict__ out, int
 #pragma unroll
             for (int k = 0; k < VEC; ++k)
                 x[k] = ptx::lds128(sbase + (uint32_t)((VEC * mr + k) * TCH + (mc ^ (mr & 7))) * 16u);
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) {
-                if (!full && VEC * mc + j >= nc) break;
-                uint4 o;
-                if constexpr (ES == 4) {        // o = column j of the 4x4 block
-                    o = make_uint4(vt_word(x[0], j), vt_word(x[1], j), vt_word(x[2], j),
-                                   vt_word(x[3], j));
-                } else {                        // 2x2 of 8-byte cells
-                    o = make_uint4(vt_word(x[0], 2 * j), vt_word(x[0], 2 * j + 1),
-                                   vt_word(x[1], 2 * j), vt_word(x[1], 2 * j + 1));
-                }
-                if (DESC_MUTANT(MUT_TILED_TILE_ONLY)) o = x[j];
-                ptx::stg128(dst + ((int64_t)(VEC * mc + j) * ld_out + VEC * mr) * ES, o);
-            }
+            // output row VEC mc + j = column j of the VEC x VEC block (micro_row,
+            // tma_transpose.cuh: register renaming for 4/8-byte cells, PRMT for 1/2-byte)
+            const int jmax = full ? VEC : min(VEC, nc - VEC * mc);
+            char *drow = dst + ((int64_t)(VEC * mc) * ld_out + VEC * mr) * ES;
+            vt_emit<ES>(x, drow, ld_out * ES, jmax, std::make_integer_sequence<int, VEC>{});
         }
         __syncthreads();                                  // staging reused by the next tile
     }

@@ -49,7 +49,7 @@ for st in "$@"; do
       echo "sanitize rc=$?"; cat gpurun_out/sanitize.log;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-          --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 5 --no-oracle --no-e2e \
+          --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 5 --no-oracle --no-e2e --no-context \
           > gpurun_out/launches_bench.log 2>&1
       echo "launches rc=$?";;
     ncu:*)
@@ -59,7 +59,7 @@ for st in "$@"; do
       rest=${st#ncu:}; w=${rest%%:*}; k=${rest#*:}
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 5 -c 1 \
           -o gpurun_out/prof_${w}_${k} -f python bench.py --workload $w --steps 8 --warmup 3 \
-          --no-oracle --no-e2e > gpurun_out/ncu_${w}_${k}.log 2>&1
+          --no-oracle --no-e2e --no-context > gpurun_out/ncu_${w}_${k}.log 2>&1
       echo "ncu $w $k rc=$?"
       python scripts/ncu_summary.py gpurun_out/prof_${w}_${k}.ncu-rep gpurun_out/ncu_${w}_${k}.md $w > /dev/null 2>&1
       cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json

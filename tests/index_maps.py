@@ -178,7 +178,7 @@ def vtiled_launch(batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, T
     """csrc/vtiled_transpose.cuh transpose_vtiled_kernel restated at element granularity.
     Tile TR = 16 VEC rows x TCH 16-byte chunks (VEC = 16 / es cells each), one NT-thread CTA
     per tile (desc_transpose.cu run_vtiled defaults: 64 x 64 cells / 128 threads for 4-byte
-    cells, 32 x 32 / 64 for 8-byte).  Copy-in: chunk q = tid + NT k -> row q / TCH, chunk
+    cells, 32 x 32 / 64 for 8-byte, 128 x 64 / 128 for 2-byte, 256 x 128 / 128 for 1-byte).  Copy-in: chunk q = tid + NT k -> row q / TCH, chunk
     q % TCH, stored at chunk (q % TCH) ^ ((row / VEC) & 7); copy-out: micro-block b = tid +
     NT m -> (mr, mc) = (b % 16, b / 16), VEC 16-byte reads of rows VEC mr + k at chunk
     mc ^ (mr & 7), output row VEC mc + j gets cells x[k][j].  mutant in {None, "tile_only"
@@ -187,7 +187,7 @@ def vtiled_launch(batch, rows, cols, ld_in, ld_out, stride_in, stride_out, es, T
     sw = 1 if swizzle else 0
     VEC = 16 // es
     if TCH is None:
-        TCH, NT = (16, 64) if es == 8 else (16, 128)
+        TCH, NT = {8: (16, 64), 4: (16, 128), 2: (8, 128), 1: (8, 128)}[es]
     TR, TC = 16 * VEC, TCH * VEC
     assert rows % VEC == 0 and cols % VEC == 0
     tiles_r, tiles_c = -(-rows // TR), -(-cols // TC)

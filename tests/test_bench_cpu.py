@@ -45,3 +45,13 @@ def test_our_arm_needs_a_gpu():
     p = _bench("--steps", "3", "--warmup", "3", "--no-oracle", "--no-e2e", timeout=120)
     assert p.returncode != 0
     assert not [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_context_measurements_run_after_the_parity_check():
+    """The same-bytes copy / graph-replay context writes into the timed output buffers, so
+    it must run after the parity check of ours_arm (an r02 ordering bug made every R = 1
+    workload report MISMATCH although the kernels were exact)."""
+    import inspect
+    import bench
+    src = inspect.getsource(bench.ours_arm)
+    assert src.index('parity = ("bit-exact vs oracle"') < src.index("live_ceiling_context(")

@@ -100,7 +100,7 @@ def _kernels_for(es, rows, cols, ld_in, ld_out):
         ks.append("tma")
         if es in (4, 8) and rows * es >= 16:
             ks += ["tma_st", "tma_tile"]
-        if es in (4, 8) and rows % (16 // es) == 0 and cols % (16 // es) == 0:
+        if rows % (16 // es) == 0 and cols % (16 // es) == 0:
             ks.append("vtiled")
     return ks
 
@@ -170,25 +170,26 @@ def test_batched_odd_strides(es):
     run_case(3, 70, 99, es, "tiled", ld_in=101, ld_out=71, stride_in=101 * 75, stride_out=71 * 99)
 
 
-@pytest.mark.parametrize("es", [4, 8])
+@pytest.mark.parametrize("es", [1, 2, 4, 8])
 def test_vtiled_shapes_and_rules(es):
-    """DESC_KERNEL_VTILED (16-byte cp.async staging, swizzled tile, register micro-transposes):
+    """DESC_KERNEL_VTILED (16-byte cp.async staging, swizzled tile, register micro-transposes;
+    4x4 / 2x2 renaming for 4/8-byte cells, 8x8 / 16x16 byte permutes for 2/1-byte cells):
     ragged edge tiles in both directions, padded ld, batched strides, the BASELINE f64 shapes;
     arguments outside its rules (misaligned base, rows or cols not a multiple of 16/size,
     ld*size not a multiple of 16) are refused with DESC_ERR_KERNEL, never run."""
     v = 16 // es
-    for rows, cols in ((68, 132), (4 * v, 260), (132, 4 * v), (v, v), (64, 64), (96, 160),
-                       (1000, 1536)):
+    for rows, cols in ((17 * v, 33 * v), (4 * v, 65 * v), (65 * v, 4 * v), (v, v), (64, 64),
+                       (6 * v, 10 * v), (1000, 1536)):
         run_case(1, rows, cols, es, "vtiled")
-    run_case(1, 68, 132, es, "vtiled", ld_in=136, ld_out=72)
-    run_case(7, 36, 64, es, "vtiled", ld_in=72, ld_out=40, stride_in=36 * 72 + v,
-             stride_out=64 * 40 + 2 * v)
+    run_case(1, 17 * v, 33 * v, es, "vtiled", ld_in=34 * v, ld_out=18 * v)
+    run_case(7, 9 * v, 16 * v, es, "vtiled", ld_in=18 * v, ld_out=10 * v,
+             stride_in=9 * v * 18 * v + v, stride_out=16 * v * 10 * v + 2 * v)
     if es == 8:
         run_case(1, 3000, 5000, es, "vtiled")
     for kw in (dict(in_off=es), dict(out_off=es)):
         with pytest.raises(desc.DescError, match="DESC_ERR_KERNEL"):
             run_case(1, 64, 64, es, "vtiled", check=False, **kw)
-    for rows, cols, ld_in, ld_out in ((67, 132, 132, 72), (68, 131, 136, 68), (68, 130, 130, 68)):
+    for rows, cols, ld_in, ld_out in ((67, 132, 144, 80), (68, 131, 144, 80), (68, 130, 130, 68)):
         if (ld_in * es) % 16 == 0 and (ld_out * es) % 16 == 0 and rows % v == 0 and cols % v == 0:
             continue
         with pytest.raises(desc.DescError, match="DESC_ERR_KERNEL"):

@@ -111,14 +111,15 @@ def _vtiled_shapes(es):
     return out
 
 
-@pytest.mark.parametrize("es", [4, 8])
+@pytest.mark.parametrize("es", [1, 2, 4, 8])
 def test_vtiled_map_is_a_race_free_conflict_free_bijection(es):
     """transpose_vtiled_kernel (csrc/vtiled_transpose.cuh), default tile per cell size and the
     DESC_VTILED_CFG alternatives: every output element once with its transpose source, no
     shared-memory race, every 8-lane phase of the 16-byte copy-in and copy-out conflict-free
     (the 16-byte XOR swizzle)."""
     cfgs = {4: [(16, 128), (16, 256), (32, 256), (8, 128), (16, 64), (32, 128), (8, 64)],
-            8: [(16, 64), (16, 256), (32, 256), (8, 128), (16, 128), (32, 128), (32, 64)]}
+            8: [(16, 64), (16, 256), (32, 256), (8, 128), (16, 128), (32, 128), (32, 64)],
+            2: [(8, 128), (16, 256), (8, 64)], 1: [(8, 128), (8, 64)]}
     for shape in _vtiled_shapes(es):
         for TCH, NT in cfgs[es]:
             L = IM.vtiled_launch(*shape, es, TCH=TCH, NT=NT)
