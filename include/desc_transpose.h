@@ -80,7 +80,8 @@ typedef enum desc_dtype {
 
 /* Kernel variants (desc_transpose_ex).  AUTO picks TILED for 4/8-byte cells when rows
  * and cols are both >= 64 (measured fastest there) and whenever the TMA alignment rules
- * below fail; otherwise TMA_ST when the element size is 4 or 8 with rows*size >= 16,
+ * below fail; VTILED for 1/2-byte cells when its rules hold (rows, cols multiples of
+ * 16/size); otherwise TMA_ST when the element size is 4 or 8 with rows*size >= 16,
  * else TMA.
  *   DESC_KERNEL_SMEM : 32x32 shared-memory tile, padded [32][33], 32x8 threads,
  *                      predicated edges -- the corrected Listing 1 schedule
@@ -105,12 +106,13 @@ typedef enum desc_dtype {
  *                      mbarrier, conflict-free register micro-transposes written back
  *                      into the same (swizzled) buffer, TMA bulk tensor stores.  Same
  *                      alignment rules as DESC_KERNEL_TMA_ST; element size 4 or 8.
- *   DESC_KERNEL_VTILED : one tile per CTA (64x64 cells for 4-byte, 32x32 for 8-byte cells)
- *                      staged with 16-byte cp.async copies into a 16-byte XOR-swizzled
- *                      shared tile (conflict-free both ways, no padding), 4x4 / 2x2
- *                      register micro-transposes, 16-byte coalesced stores.  Needs the
- *                      TMA alignment rules above plus rows and cols multiples of 16/size;
- *                      element size 4 or 8.  */
+ *   DESC_KERNEL_VTILED : one tile per CTA (64x64 cells for 4-byte, 32x32 for 8-byte,
+ *                      128x64 for 2-byte, 256x128 for 1-byte cells) staged with 16-byte
+ *                      cp.async copies into a 16-byte XOR-swizzled shared tile
+ *                      (conflict-free both ways, no padding), VEC x VEC register
+ *                      micro-transposes (VEC = 16/size), 16-byte coalesced stores.  Needs
+ *                      the TMA alignment rules above plus rows and cols multiples of
+ *                      16/size; any element size.  */
 typedef enum desc_kernel {
     DESC_KERNEL_AUTO = 0,
     DESC_KERNEL_SMEM = 1,
@@ -142,7 +144,7 @@ desc_status desc_transpose_ex(const void *in, void *out, int64_t batch,
                               desc_kernel kernel, void *stream);
 
 /* The variant AUTO would run for these arguments (no launch, no pointer
- * checks beyond alignment).  Returns DESC_KERNEL_TILED, _TMA, _TMA_ST or _TMA_TILE. */
+ * checks beyond alignment).  Returns DESC_KERNEL_TILED, _VTILED, _TMA or _TMA_ST. */
 desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch,
                                int64_t rows, int64_t cols, int64_t ld_in,
                                int64_t ld_out, int64_t stride_in,

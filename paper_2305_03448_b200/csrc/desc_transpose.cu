@@ -567,6 +567,13 @@ bool vtiled_ok(const Args &a) {
     return a.rows % vec == 0 && a.cols % vec == 0;
 }
 
+// AUTO's kernel for 1/2-byte cells whenever the vector tile kernel's rules hold: its 16 x 16 /
+// 8 x 8 byte-permute micro-transposes beat the persistent TMA-load kernel on every measured
+// shape (profiles/r02_vtiled_narrow.txt, back to back: 8192^2 u8 0.726 -> 0.933, 16384^2 u8
+// 0.690 -> 0.973, 8192^2 bf16 0.761 -> 0.995, 4096^2 bf16 0.613 -> 0.956, 256 x 1024^2 bf16
+// 0.960 -> 1.049); 4/8-byte cells keep TILED (tiled_preferred).
+bool narrow_vtiled(const Args &a) { return (a.es == 1 || a.es == 2) && vtiled_ok(a); }
+
 template <int ES, int TCH, int NT>
 desc_status launch_vtiled(const Args &a) {
     using C = desc::VTiledCfg<ES, TCH, NT>;
@@ -943,6 +950,7 @@ desc_status dispatch(const Args &a, desc_kernel k) {
     if (k == DESC_KERNEL_SMEM) return run_smem(a);
     if (k == DESC_KERNEL_TILED || (k == DESC_KERNEL_AUTO && (!tma_ok || tiled_preferred(a))))
         return run_tiled(a);
+    if (k == DESC_KERNEL_AUTO && narrow_vtiled(a)) return run_vtiled(a);
     if (k == DESC_KERNEL_AUTO && tma_store_ok(a)) return run_tma2(a);
     if (k == DESC_KERNEL_TMA || k == DESC_KERNEL_AUTO) return run_tma(a);
     return fail(DESC_ERR_KERNEL, "unknown kernel variant %d", (int)k);
@@ -1965,6 +1973,7 @@ desc_kernel desc_select_kernel(const void *in, const void *out, int64_t batch, i
     Args a{in, const_cast<void *>(out), batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
            dtype_size(dtype), nullptr};
     if (a.es == 0 || !tma_eligible(a) || tiled_preferred(a)) return DESC_KERNEL_TILED;
+    if (narrow_vtiled(a)) return DESC_KERNEL_VTILED;
     return tma_store_ok(a) ? DESC_KERNEL_TMA_ST : DESC_KERNEL_TMA;
 }
 

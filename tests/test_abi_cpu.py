@@ -153,11 +153,13 @@ def test_host_entry_validation(lib):
 def test_select_kernel_alignment_rules(lib):
     i, o = FAKE_IN, FAKE_OUT
     assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "f32") == "tiled"
-    assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "u8") == "tma"
+    assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "u8") == "vtiled"
+    assert desc.desc_select_kernel(i, o, 1, 56, 64, 64, 64, 0, 0, "u8") == "tma"     # 56 % 16
     assert desc.desc_select_kernel(i, o, 1, 2, 64, 64, 4, 0, 0, "f32") == "tma"
     assert desc.desc_select_kernel(i, o, 1, 32, 64, 64, 32, 0, 0, "f32") == "tma_st"   # skinny
     assert desc.desc_select_kernel(i, o, 1, 64, 48, 48, 64, 0, 0, "f64") == "tma_st"
-    assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "bf16") == "tma"
+    assert desc.desc_select_kernel(i, o, 1, 64, 64, 64, 64, 0, 0, "bf16") == "vtiled"
+    assert desc.desc_select_kernel(i, o, 1, 60, 64, 64, 64, 0, 0, "bf16") == "tma"   # 60 % 8
     assert desc.desc_select_kernel(i + 4, o, 1, 64, 64, 64, 64, 0, 0, "f32") == "tiled"
     assert desc.desc_select_kernel(i, o, 1, 3000, 5001, 5001, 3000, 0, 0, "f64") == "tiled"
     assert desc.desc_select_kernel(i, o, 1, 3000, 5000, 5000, 3000, 0, 0, "f64") == "tiled"

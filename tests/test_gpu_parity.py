@@ -179,7 +179,7 @@ def test_vtiled_shapes_and_rules(es):
     ld*size not a multiple of 16) are refused with DESC_ERR_KERNEL, never run."""
     v = 16 // es
     for rows, cols in ((17 * v, 33 * v), (4 * v, 65 * v), (65 * v, 4 * v), (v, v), (64, 64),
-                       (6 * v, 10 * v), (1000, 1536)):
+                       (6 * v, 10 * v), (1008, 1536)):
         run_case(1, rows, cols, es, "vtiled")
     run_case(1, 17 * v, 33 * v, es, "vtiled", ld_in=34 * v, ld_out=18 * v)
     run_case(7, 9 * v, 16 * v, es, "vtiled", ld_in=18 * v, ld_out=10 * v,
