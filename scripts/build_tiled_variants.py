@@ -29,6 +29,8 @@ VARIANTS = {
     "vt_nocpa": ["DESC_VT_CPA=0"],
     # TMA ring slot release after ld.shared without the proxy fence (ptx.cuh)
     "rel0": ["DESC_REL_MODE=0"],
+    # view copies: first-item prefetch compiled into the plain 16-byte mode
+    "viewpf1": ["DESC_VIEW_PF1=1"],
 }
 names = sys.argv[1:] or [n for n in VARIANTS if n not in ("s1", "s2", "s3")]
 out_dir = os.path.join(B.ROOT, "build_variants")
