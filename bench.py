@@ -1379,7 +1379,8 @@ def measure_e2e(args, desc, torch, dev, stream, src_t, tdt, batch, rows, cols, w
     es = wl["es"]
     h_in = src_t.pin_memory()
     h_out = torch.empty((batch, cols, rows), dtype=src_t.dtype).pin_memory()
-    nbytes_ws = desc.desc_transpose_host_workspace(rows, cols, wl["dtype"])
+    nbytes_ws = (desc.desc_transpose_host_workspace_batched(batch, rows, cols, wl["dtype"])
+                 if batch > 1 else desc.desc_transpose_host_workspace(rows, cols, wl["dtype"]))
     work = torch.empty(nbytes_ws, dtype=torch.uint8, device=dev)
     nbytes = batch * rows * cols * es
     steps = max(3, min(args.steps, args.e2e_steps))

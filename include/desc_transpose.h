@@ -311,6 +311,14 @@ size_t desc_read_probe_sink_bytes(void);
  * or 512-row bands if larger). */
 size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtype);
 
+/* Recommended workspace bytes for a BATCHED desc_transpose_host call whose matrices are
+ * stored back to back with a tight output (stride_in = rows*ld_in, ld_out = rows, stride_out
+ * = cols*rows): room for whole-matrix bands of ~32 MB of input (at least 8 bands), which move
+ * each band with one contiguous H2D and one contiguous D2H copy.  Never less than
+ * desc_transpose_host_workspace(rows, cols, dtype). */
+size_t desc_transpose_host_workspace_batched(int64_t batch, int64_t rows, int64_t cols,
+                                             desc_dtype dtype);
+
 /* Number of kernel launches the last successful call of this thread issued (0 for an
  * empty shape, 1 per device call, one per band for desc_transpose_host). */
 int desc_last_launch_count(void);

@@ -26,6 +26,7 @@ __all__ = [
     "desc_scan_workspace", "SCAN_ALGO", "desc_read_probe", "desc_read_probe_sink_bytes",
     "desc_slab_transpose_peer",
     "block_reduce", "scan", "desc_transpose_host_workspace",
+    "desc_transpose_host_workspace_batched",
     "transpose", "transpose_batched", "transpose_host",
 ]
 
@@ -92,6 +93,8 @@ def load():
     lib.desc_transpose_host.restype = ci
     lib.desc_transpose_host_workspace.argtypes = [i64, i64, ci]
     lib.desc_transpose_host_workspace.restype = ctypes.c_size_t
+    lib.desc_transpose_host_workspace_batched.argtypes = [i64, i64, i64, ci]
+    lib.desc_transpose_host_workspace_batched.restype = ctypes.c_size_t
     lib.desc_copy_batched.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci, vp]
     lib.desc_copy_batched.restype = ci
     lib.desc_ipc_handle.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
@@ -177,6 +180,10 @@ def desc_transpose_host(h_in_ptr, h_out_ptr, batch, rows, cols, ld_in, ld_out, s
 
 def desc_transpose_host_workspace(rows, cols, dtype) -> int:
     return load().desc_transpose_host_workspace(rows, cols, _dt(dtype))
+
+
+def desc_transpose_host_workspace_batched(batch, rows, cols, dtype) -> int:
+    return load().desc_transpose_host_workspace_batched(batch, rows, cols, _dt(dtype))
 
 
 def desc_copy_batched(in_ptr, out_ptr, batch, rows, cols, ld_in, ld_out, stride_in, stride_out,
@@ -415,7 +422,7 @@ def transpose_host(x, out=None, work=None):
     if tuple(o3.shape) != (batch, cols, rows) or out.dtype != x.dtype:
         raise ValueError("out has the wrong shape or dtype")
     if work is None:
-        nbytes = desc_transpose_host_workspace(rows, cols, x.dtype)
+        nbytes = desc_transpose_host_workspace_batched(batch, rows, cols, x.dtype)
         work = torch.empty(max(nbytes, 256), dtype=torch.uint8, device="cuda")
     ld_in = x3.stride(1) if rows > 1 else cols
     ld_out = o3.stride(1) if cols > 1 else rows

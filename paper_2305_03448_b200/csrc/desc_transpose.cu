@@ -1107,6 +1107,61 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
         return fail(DESC_ERR_SHAPE, "d_work (%zu bytes) too small: need >= %lld", work_bytes,
                     (long long)band_bytes(1, other, es));
 
+    // Batch bands: matrices back to back on both sides (stride_in = rows * ld_in; a tight
+    // output, ld_out = rows and stride_out = cols * rows, so that no output padding byte is
+    // ever written, R8) travel whole -- each band is nb consecutive matrices: ONE contiguous
+    // H2D copy, one batched transpose, ONE contiguous D2H copy, no strided rows on either side
+    // of PCIe (256 x 1024^2 f32: zero-copy 76.7 GB/s -> see profiles/r02_exp_e2e_batch.txt).
+    // At least 8 bands when the batch allows.  DESC_HOST_BATCH=0 turns it off (A/B).
+    static const int batch_bands = dev_knob("DESC_HOST_BATCH", 1);
+    static const int host_mode = dev_knob("DESC_HOST_MODE", 0);
+    if (batch_bands && batch > 1 && host_mode != 2 && stride_in == rows * ld_in &&
+        ld_out == rows && stride_out == cols * rows) {
+        const int64_t in_m = rows * ld_in * es, out_m = cols * rows * es;   // bytes per matrix
+        int64_t nb = (int64_t)work_bytes / (2 * (round_up(in_m, 256) + round_up(out_m, 256)));
+        const int64_t cap = (batch + 7) / 8;
+        if (nb > cap) nb = cap;
+        if (nb >= 1) {
+            HostPipe *hp;
+            if (desc_status s = host_pipe(dev, &hp)) return s;
+            char *w = static_cast<char *>(d_work);
+            const int64_t in_b = round_up(nb * in_m, 256), out_b = round_up(nb * out_m, 256);
+            char *d_in[2] = {w, w + in_b};
+            char *d_out[2] = {w + 2 * in_b, w + 2 * in_b + out_b};
+            if ((e = cudaEventRecord(hp->enter, stream)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+            for (int i = 0; i < 2; ++i)
+                if ((e = cudaStreamWaitEvent(hp->s[i], hp->enter, 0)) != cudaSuccess)
+                    return cuda_fail(e, "cudaStreamWaitEvent");
+            int launches = 0;
+            int64_t k = 0;
+            for (int64_t b0 = 0; b0 < batch; b0 += nb, ++k) {
+                const int64_t m = batch - b0 < nb ? batch - b0 : nb;
+                const int buf = (int)(k & 1);
+                cudaStream_t s = hp->s[buf];
+                // the last matrix's last row ends at cols (its pitch padding may lie outside
+                // the caller's buffer)
+                const int64_t nin = m * in_m - (ld_in - cols) * es;
+                e = cudaMemcpyAsync(d_in[buf], static_cast<const char *>(h_in) + b0 * in_m, nin,
+                                    cudaMemcpyHostToDevice, s);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+                Args a{d_in[buf], d_out[buf], m, rows, cols, ld_in, rows, rows * ld_in, cols * rows,
+                       es, s};
+                if (desc_status st = dispatch(a, DESC_KERNEL_AUTO)) return st;
+                ++launches;
+                e = cudaMemcpyAsync(static_cast<char *>(h_out) + b0 * out_m, d_out[buf], m * out_m,
+                                    cudaMemcpyDeviceToHost, s);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+            }
+            for (int i = 0; i < 2; ++i) {
+                if ((e = cudaEventRecord(hp->done[i], hp->s[i])) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+                if ((e = cudaStreamWaitEvent(stream, hp->done[i], 0)) != cudaSuccess)
+                    return cuda_fail(e, "cudaStreamWaitEvent");
+            }
+            g_last_launches = launches;
+            return DESC_OK;
+        }
+    }
+
     // Zero-copy mode: when both host buffers are page-locked and mapped, the TILED kernel
     // reads the input and writes the transposed output straight over PCIe in one pass.
     // SM loads / stores reach 51 / 53 GB/s per direction and 80 GB/s both ways at once
@@ -1114,7 +1169,6 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     // profiles/r01_exp_zerocopy.txt), so AUTO keeps the banded copy pipeline unless it
     // would be cut into many small copies (> 64 bands, e.g. 256 x 1024^2: 62 GB/s banded vs
     // 75 GB/s zero-copy).  DESC_HOST_MODE=1 forces bands, =2 forces zero-copy (A/B).
-    static const int host_mode = dev_knob("DESC_HOST_MODE", 0);
     const int64_t nbands = batch * ((span + band - 1) / band);
     void *dz_in = nullptr, *dz_out = nullptr;
     if ((host_mode == 2 || (host_mode == 0 && nbands > 64)) && mapped_host(h_in, &dz_in) &&
@@ -1995,6 +2049,23 @@ size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtyp
     const int64_t br = rows < 512 ? rows : 512, bc = cols < 1024 ? cols : 1024;
     const int64_t a = band_bytes(br, cols, es), b = band_bytes(bc, rows, es);
     return (size_t)(a > b ? a : b);
+}
+
+size_t desc_transpose_host_workspace_batched(int64_t batch, int64_t rows, int64_t cols,
+                                             desc_dtype dtype) {
+    const size_t one = desc_transpose_host_workspace(rows, cols, dtype);
+    const int es = dtype_size(dtype);
+    if (es == 0 || batch <= 1 || rows <= 0 || cols <= 0) return one;
+    // whole-matrix bands (run_host): ~32 MB of input per band and at least 8 bands
+    // (scripts/exp_e2e_batch.py, 256 x 1024^2 f32: 4 / 16 / 32 matrices per band 92.5 /
+    // 93.1 / 90.0 GB/s against 77 GB/s for one matrix per band or the zero-copy path)
+    const int64_t in_m = round_up(rows * cols * es, 256), out_m = in_m;
+    int64_t nb = ((int64_t)32 << 20) / in_m;
+    if (nb < 1) nb = 1;
+    const int64_t cap = (batch + 7) / 8;
+    if (nb > cap) nb = cap;
+    const size_t want = (size_t)(2 * nb * (in_m + out_m));
+    return want > one ? want : one;
 }
 
 desc_status desc_ipc_handle(const void *dptr, void *handle_out, uint64_t *offset_out) {

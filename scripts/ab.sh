@@ -1,6 +1,6 @@
 #!/bin/bash
 # Named A/B experiments of round 2 (each was a one-off driver; folded here).
-#   bash scripts/ab.sh <name> [args...]      names: tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
+#   bash scripts/ab.sh <name> [args...]      names: e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
 # Compile-time variants come from scripts/build_{tiled,scan}_variants.py (DESC_LIB=...);
 # each experiment prints the lines its profiles/r02_*.txt record holds.
 
@@ -154,5 +154,13 @@ f64_2048() {
   done
 }
 
+e2e_batch() {
+  # r02 (session 2): batched e2e -- whole-matrix bands (contiguous copies) vs the previous
+  # zero-copy path (DESC_HOST_BATCH=0)
+  for r in 1 2; do for b in 1 0; do
+    DESC_HOST_BATCH=$b python bench.py --workload batched --steps 20 --warmup 5 --no-oracle --no-context 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); e=d['e2e']; print('batch_bands=$b', e['value'], e['pcie_ceiling']['frac'], e['spot_check'], e['gpu_launches'])"
+  done; done
+}
+
 name=$1; shift
-case " tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac
+case " e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac

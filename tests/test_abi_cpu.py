@@ -148,6 +148,13 @@ def test_host_entry_validation(lib):
     # double-buffered 1024-column bands (in: 8192 x 1024, out: 1024 x 8192), r02 band axis
     assert desc.desc_transpose_host_workspace(8192, 8192, "f32") == 2 * 2 * 1024 * 8192 * 4
     assert desc.desc_transpose_host_workspace(0, 8, "f32") == 0
+    # batched: ~32 MB of input per whole-matrix band, >= 8 bands, never below the 1-matrix size
+    assert desc.desc_transpose_host_workspace_batched(256, 1024, 1024, "f32") == 2 * 8 * 2 * (4 << 20)
+    assert desc.desc_transpose_host_workspace_batched(16, 1024, 1024, "f32") == 2 * 2 * 2 * (4 << 20)
+    assert desc.desc_transpose_host_workspace_batched(1, 1024, 1024, "f32") == \
+        desc.desc_transpose_host_workspace(1024, 1024, "f32")
+    # matrices above 32 MB travel one per band (in + out, double-buffered)
+    assert desc.desc_transpose_host_workspace_batched(64, 8192, 8192, "f32") == 2 * 2 * (256 << 20)
 
 
 def test_select_kernel_alignment_rules(lib):

@@ -456,18 +456,52 @@ print("ok")
 
 def test_transpose_host_zero_copy_many_bands():
     """> 64 bands with pinned (mapped) host buffers: one TILED launch over PCIe reads and
-    writes the host buffers directly; pageable buffers keep the banded copy pipeline."""
+    writes the host buffers directly; pageable buffers keep the banded copy pipeline.  The
+    output has padded rows (ld_out > rows), so the batch-band path (tight outputs only) does
+    not apply, and the padding must survive."""
     src = synth.random_bits((80, 70, 50), 4, 123)
     for pinned in (True, False):
         x = torch.from_numpy(src.view(np.int32))
+        big = torch.full((80, 50, 72), -1, dtype=torch.int32)
         if pinned:
-            x = x.pin_memory()
+            x, big = x.pin_memory(), big.pin_memory()
         nbytes = desc.desc_transpose_host_workspace(64, 50, "i32")
         work = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-        y = desc.transpose_host(x, work=work)
+        desc.transpose_host(x, out=big[:, :, :70], work=work)
         torch.cuda.synchronize()
         assert desc.desc_last_launch_count() == (1 if pinned else 160)
-        assert y.numpy().view(np.uint32).tobytes() == oracle.transpose(src).tobytes()
+        got = big.numpy()
+        assert got[:, :, :70].view(np.uint32).tobytes() == oracle.transpose(src).tobytes()
+        assert (got[:, :, 70:] == -1).all()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_transpose_host_batch_bands(pinned):
+    """Matrices stored back to back with a tight output travel whole: each band is a group of
+    consecutive matrices -- one contiguous H2D copy, one batched transpose, one contiguous D2H
+    copy; also with a padded input pitch (the last row's padding may lie past the buffer)."""
+    # (the default workspace holds one whole tight matrix when cols <= 1024; a padded pitch or
+    # a larger matrix falls back to column bands -- parity either way)
+    for (batch, rows, cols, ld_in, whole) in ((80, 70, 50, 50, True), (33, 64, 96, 96, True),
+                                              (33, 64, 96, 100, False),
+                                              (9, 1000, 1536, 1536, False)):
+        full = synth.random_bits((batch, rows, ld_in), 4, batch + rows)
+        src = full[:, :, :cols]
+        flat = full.reshape(-1)[:(batch * rows - 1) * ld_in + cols].copy()   # ends at the last cell
+        x = torch.from_numpy(flat.view(np.int32))
+        out = torch.empty((batch, cols, rows), dtype=torch.int32)
+        if pinned:
+            x, out = x.pin_memory(), out.pin_memory()
+        nbytes = desc.desc_transpose_host_workspace(rows, cols, "i32")
+        work = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        desc.desc_transpose_host(x.data_ptr(), out.data_ptr(), batch, rows, cols, ld_in, rows,
+                                 rows * ld_in, cols * rows, "i32", work.data_ptr(), nbytes,
+                                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        n = desc.desc_last_launch_count()
+        if whole:
+            assert min(batch, 8) <= n <= batch, n
+        assert out.numpy().view(np.uint32).tobytes() == oracle.transpose(np.ascontiguousarray(src)).tobytes()
 
 
 def test_transpose_host_rejects_device_buffers():
