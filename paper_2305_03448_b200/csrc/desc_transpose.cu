@@ -992,10 +992,11 @@ desc_status run(const Args &a, desc_kernel k) {
 // copy of band k+1, the transpose of band k and the D2H copy of band k-1 overlap (PCIe is
 // full duplex).  The caller's stream is joined at entry and exit with events, so the call
 // stays asynchronous and ordered on `stream`.
+constexpr int kHostStreams = 3;          // internal streams (2 or 3 used, DESC_HOST_STREAMS)
 struct HostPipe {
     bool init = false;
-    cudaStream_t s[2];
-    cudaEvent_t enter, done[2];
+    cudaStream_t s[kHostStreams];
+    cudaEvent_t enter, done[kHostStreams];
 };
 std::mutex g_pipe_mu;
 HostPipe g_pipe[64];
@@ -1005,7 +1006,7 @@ desc_status host_pipe(int dev, HostPipe **out) {
     HostPipe &hp = g_pipe[dev];
     if (!hp.init) {
         cudaError_t e;
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostStreams; ++i) {
             if ((e = cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(e, "cudaStreamCreateWithFlags");
             if ((e = cudaEventCreateWithFlags(&hp.done[i], cudaEventDisableTiming)) != cudaSuccess)
@@ -1096,16 +1097,21 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     // at most span / DESC_HOST_BANDS (default 8, rounded up to 128): with fewer, larger
     // bands the one-way fill (first H2D) and drain (last D2H) dominate small matrices
     static const int min_bands = dev_knob("DESC_HOST_BANDS", 8);
+    // NBUF band buffers on as many internal streams: 2 (double buffering), or 3 with
+    // DESC_HOST_STREAMS=3 (A/B; the H2D of band k+2 then never waits for the D2H of band k)
+    static const int nbuf_knob = dev_knob("DESC_HOST_STREAMS", 2);
+    const int NBUF = nbuf_knob == 3 ? 3 : 2;
+    auto fits = [&](int64_t b) { return band_bytes(b, other, es) / 2 * NBUF <= (int64_t)work_bytes; };
     int64_t band = span;
     if (min_bands > 1) {
         const int64_t cap = round_up((span + min_bands - 1) / min_bands, 128);
         if (cap < band) band = cap;
     }
-    while (band > 1 && band_bytes(band, other, es) > (int64_t)work_bytes)
+    while (band > 1 && !fits(band))
         band = band > 256 ? (band / 2 + 127) / 128 * 128 : band / 2;
-    if (band_bytes(band, other, es) > (int64_t)work_bytes)
+    if (!fits(band))
         return fail(DESC_ERR_SHAPE, "d_work (%zu bytes) too small: need >= %lld", work_bytes,
-                    (long long)band_bytes(1, other, es));
+                    (long long)(band_bytes(1, other, es) / 2 * NBUF));
 
     // Batch bands: matrices back to back on both sides (stride_in = rows * ld_in; a tight
     // output, ld_out = rows and stride_out = cols * rows, so that no output padding byte is
@@ -1188,11 +1194,14 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
     const int64_t narrow = round_up(other * round_up(band, v) * es, 256);
     const int64_t in_b = by_cols ? narrow : wide, out_b = by_cols ? wide : narrow;
     char *w = static_cast<char *>(d_work);
-    char *d_in[2] = {w, w + in_b};
-    char *d_out[2] = {w + 2 * in_b, w + 2 * in_b + out_b};
+    char *d_in[kHostStreams], *d_out[kHostStreams];
+    for (int i = 0; i < NBUF; ++i) {
+        d_in[i] = w + i * in_b;
+        d_out[i] = w + NBUF * in_b + i * out_b;
+    }
 
     if ((e = cudaEventRecord(hp->enter, stream)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < NBUF; ++i)
         if ((e = cudaStreamWaitEvent(hp->s[i], hp->enter, 0)) != cudaSuccess)
             return cuda_fail(e, "cudaStreamWaitEvent");
     int launches = 0;
@@ -1202,7 +1211,7 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
             // fixed bands: measured 81 GB/s vs 77 GB/s with bands ramped at both ends
             // (scripts/exp_e2e_ramp.py; narrow bands make the strided rows short)
             const int64_t np_ = span - p0 < band ? span - p0 : band;
-            const int buf = (int)(k & 1);
+            const int buf = (int)(k % NBUF);
             cudaStream_t s = hp->s[buf];
             // this band's sub-matrix: nr x nc input cells at (r0, c0)
             const int64_t r0 = by_cols ? 0 : p0, c0 = by_cols ? p0 : 0;
@@ -1222,7 +1231,7 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync D2H");
         }
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
         if ((e = cudaEventRecord(hp->done[i], hp->s[i])) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
         if ((e = cudaStreamWaitEvent(stream, hp->done[i], 0)) != cudaSuccess)
             return cuda_fail(e, "cudaStreamWaitEvent");
