@@ -83,6 +83,9 @@ struct CellIO {
 // MODE 0: element cells (Cell), any s1.   MODE 1: 16-byte cells, s1 = +1.
 // MODE 2: 16-byte cells, s1 = -1 (mirrored load + in-register element reversal).
 // Short rows: up to 4 rows' loads are in flight per thread before their stores.
+#ifndef DESC_VIEW_UNR         // rows' loads in flight per thread in the short-row path (A/B)
+#define DESC_VIEW_UNR 4
+#endif
 #ifndef DESC_VIEW_PF1         // A/B: compile the first-item prefetch into MODE 1 too
 #define DESC_VIEW_PF1 0
 #endif
@@ -134,15 +137,15 @@ view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const Vie
         if (u1 - u0 <= uw) {                  // one cell per thread per row: unroll rows
             const int64_t u = u0 + tu;
             const bool uok = u < u1;
-            for (int64_t r = r0 + tr; r < r1; r += 4 * rpp) {
-                T c[4];
+            for (int64_t r = r0 + tr; r < r1; r += DESC_VIEW_UNR * rpp) {
+                T c[DESC_VIEW_UNR];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < DESC_VIEW_UNR; ++k) {
                     const int64_t rr = r + k * rpp;
                     if (uok && rr < r1) c[k] = IO::load(in, obase + rr * v.s2, u, v.s1, es);
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < DESC_VIEW_UNR; ++k) {
                     const int64_t rr = r + k * rpp;
                     if (uok && rr < r1) *reinterpret_cast<T *>(oitem + (rr * v.U + u) * CB) = c[k];
                 }

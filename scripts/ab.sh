@@ -1,6 +1,6 @@
 #!/bin/bash
 # Named A/B experiments of round 2 (each was a one-off driver; folded here).
-#   bash scripts/ab.sh <name> [args...]      names: e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
+#   bash scripts/ab.sh <name> [args...]      names: view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
 # Compile-time variants come from scripts/build_{tiled,scan}_variants.py (DESC_LIB=...);
 # each experiment prints the lines its profiles/r02_*.txt record holds.
 
@@ -162,5 +162,16 @@ e2e_batch() {
   done; done
 }
 
+view_unroll() {
+  # r02 (session 2): view copies, loads in flight per thread in the short-row path (4 default)
+  for r in 1 2; do
+    for lib in paper_2305_03448_b200/libdesc_transpose.so build_variants/lib_tiled_viewunr8.so build_variants/lib_tiled_viewunr2.so; do
+      for w in view_tiles8192f32 view_flip8192f32; do
+        DESC_LIB=$lib python bench.py --workload $w --steps 20 --warmup 5 --no-e2e --no-context 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$(basename $lib .so)', '$w', d['value'], d['roofline']['frac'], d['parity'])"
+      done
+    done
+  done
+}
+
 name=$1; shift
-case " e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac
+case " view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac

@@ -31,6 +31,8 @@ VARIANTS = {
     "rel0": ["DESC_REL_MODE=0"],
     # view copies: first-item prefetch compiled into the plain 16-byte mode
     "viewpf1": ["DESC_VIEW_PF1=1"],
+    "viewunr8": ["DESC_VIEW_UNR=8"],
+    "viewunr2": ["DESC_VIEW_UNR=2"],
 }
 names = sys.argv[1:] or [n for n in VARIANTS if n not in ("s1", "s2", "s3")]
 out_dir = os.path.join(B.ROOT, "build_variants")
