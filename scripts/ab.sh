@@ -1,6 +1,6 @@
 #!/bin/bash
 # Named A/B experiments of round 2 (each was a one-off driver; folded here).
-#   bash scripts/ab.sh <name> [args...]      names: view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
+#   bash scripts/ab.sh <name> [args...]      names: vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
 # Compile-time variants come from scripts/build_{tiled,scan}_variants.py (DESC_LIB=...);
 # each experiment prints the lines its profiles/r02_*.txt record holds.
 
@@ -173,5 +173,14 @@ view_unroll() {
   done
 }
 
+vtiled_minb() {
+  # r02 (session 2): VTILED residency (register caps via __launch_bounds__ min blocks)
+  S=8192x8192:f32,4096x4096:f32,256x1024x1024:f32,8192x8192:f64,3000x5000:f64
+  for r in 1 2; do
+    python scripts/exp_kernels.py --kernels tiled,vtiled --shapes $S
+    for v in vtminb10 vtminb12; do DESC_LIB=build_variants/lib_tiled_$v.so python scripts/exp_kernels.py --kernels vtiled --shapes $S; done
+  done
+}
+
 name=$1; shift
-case " view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac
+case " vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac

@@ -32,6 +32,8 @@ VARIANTS = {
     # view copies: first-item prefetch compiled into the plain 16-byte mode
     "viewpf1": ["DESC_VIEW_PF1=1"],
     "viewunr8": ["DESC_VIEW_UNR=8"],
+    "vtminb10": ["DESC_VT_MINB=10"],
+    "vtminb12": ["DESC_VT_MINB=12"],
     "viewunr2": ["DESC_VIEW_UNR=2"],
 }
 names = sys.argv[1:] or [n for n in VARIANTS if n not in ("s1", "s2", "s3")]
