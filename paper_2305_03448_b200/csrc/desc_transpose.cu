@@ -997,6 +997,11 @@ struct HostPipe {
     bool init = false;
     cudaStream_t s[kHostStreams];
     cudaEvent_t enter, done[kHostStreams];
+    // Held for a whole call's enqueue: the join events are shared, and an event wait
+    // snapshots the most recent record, so record -> wait must not interleave with another
+    // host thread's call on the same device (the internal streams themselves may be shared:
+    // each call's work is stream-ordered after its own entry join).
+    std::mutex enqueue;
 };
 std::mutex g_pipe_mu;
 HostPipe g_pipe[64];
@@ -1130,6 +1135,7 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
         if (nb >= 1) {
             HostPipe *hp;
             if (desc_status s = host_pipe(dev, &hp)) return s;
+            std::lock_guard<std::mutex> lk(hp->enqueue);
             char *w = static_cast<char *>(d_work);
             const int64_t in_b = round_up(nb * in_m, 256), out_b = round_up(nb * out_m, 256);
             char *d_in[2] = {w, w + in_b};
@@ -1187,6 +1193,7 @@ desc_status run_host(const void *h_in, void *h_out, int64_t batch, int64_t rows,
 
     HostPipe *hp;
     if (desc_status s = host_pipe(dev, &hp)) return s;
+    std::lock_guard<std::mutex> lk(hp->enqueue);
     const int64_t v = 16 / es;
     // row bands: band x cols in, cols x band out; column bands: rows x band in, band x rows
     // out (each 16-byte padded; the two together are what band_bytes counts)

@@ -538,3 +538,36 @@ def test_repeated_launches_8192_no_intermittent_mismatch(kernel):
             if cnt:
                 bad.append((it, cnt))
     assert not bad, f"{kernel}: launches with mismatching elements (iteration, count): {bad[:5]}"
+
+
+def test_transpose_host_two_threads():
+    """Two host threads calling desc_transpose_host at once on their own CUDA streams: the
+    per-device internal streams and join events are shared, so each call's enqueue is
+    serialised (HostPipe::enqueue); both results must be exact, every time."""
+    import threading
+    srcs = [synth.random_bits((1000, 1536), 4, 40 + k) for k in range(2)]
+    errs = []
+
+    def worker(k):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            x = torch.from_numpy(srcs[k].view(np.int32)).pin_memory()
+            work = torch.empty(desc.desc_transpose_host_workspace(1000, 1536, "i32"),
+                               dtype=torch.uint8, device="cuda")
+            for it in range(20):
+                out = torch.full((1536, 1000), -1, dtype=torch.int32).pin_memory()
+                desc.desc_transpose_host(x.data_ptr(), out.data_ptr(), 1, 1000, 1536, 1536, 1000,
+                                         0, 0, "i32", work.data_ptr(), work.numel(), s.cuda_stream)
+                s.synchronize()
+                if out.numpy().view(np.uint32).tobytes() != oracle.transpose(srcs[k]).tobytes():
+                    errs.append((k, it))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
