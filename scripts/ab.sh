@@ -1,6 +1,6 @@
 #!/bin/bash
 # Named A/B experiments of round 2 (each was a one-off driver; folded here).
-#   bash scripts/ab.sh <name> [args...]      names: vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
+#   bash scripts/ab.sh <name> [args...]      names: tiled_128rows vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
 # Compile-time variants come from scripts/build_{tiled,scan}_variants.py (DESC_LIB=...);
 # each experiment prints the lines its profiles/r02_*.txt record holds.
 
@@ -182,5 +182,15 @@ vtiled_minb() {
   done
 }
 
+tiled_128rows() {
+  # r02 (session 2): TILED f32 tiles with 128 rows (512-byte output row segments): cfg 7 =
+  # 128x64/256 thr, 8 = 128x128/512, 9 = 128x32/128 against the 64x64/256 default
+  # (needs those cases back in run_tiled, desc_transpose.cu; removed after the recorded run)
+  for r in 1 2; do for c in 0 7 8 9; do
+    DESC_TILED_CFG=$c python bench.py --steps 20 --warmup 5 --no-oracle --no-e2e --no-context 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('cfg$c 8192f32', d['value'], d['roofline']['frac'], d['parity'])"
+    DESC_TILED_CFG=$c python scripts/exp_kernels.py --kernels tiled --shapes 4096x4096:f32,256x1024x1024:f32 | sed "s/^/cfg$c /"
+  done; done
+}
+
 name=$1; shift
-case " vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac
+case " tiled_128rows vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac
