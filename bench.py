@@ -1003,10 +1003,9 @@ def dist_e2e(world, rank, dev, n, steps: int = 5):
                                      lay.M, 0, 0, "f32", hws.data_ptr(), hws.numel(),
                                      torch.cuda.current_stream(dev).cuda_stream)
             return desc.desc_last_launch_count()
-        x.copy_(h_in, non_blocking=True)
-        ddist.slab_transpose(x, out, workspace=ws, all_to_all=a2a)
-        h_out.copy_(out, non_blocking=True)
-        return 2 * ddist.default_chunks(lay.Rm, world) if world > 1 else 1
+        # the host-buffer pipeline: H2D chunks, the chunked exchange, 2-D D2H stripes
+        ddist.slab_transpose_host(h_in, h_out, x, out, workspace=ws, all_to_all=a2a)
+        return 2 * ddist.default_host_chunks(lay.Rm, 4)
     ms, launches, _ = timed_region(step, steps, 3, dev, world)
     out.copy_(h_out)                   # what reached the host, verified on the device
     parity = slab_verify(lay, out, dev, blocks=1)
@@ -1020,8 +1019,9 @@ def dist_e2e(world, rank, dev, n, steps: int = 5):
             "steps": steps, "gpu_launches": launches, "parity": parity,
             "path": ("pinned host matrix -> desc_transpose_host (banded H2D | transpose | "
                      "D2H) -> pinned host, every step" if world == 1 else
-                     "pinned host slab -> H2D -> slab_transpose (public API) -> D2H -> pinned "
-                     "host slab, every step")}
+                     "pinned host slab -> dist.slab_transpose_host (H2D of row chunks | "
+                     "chunked transpose + all-to-all + unpack | 2-D D2H of the output column "
+                     "stripes) -> pinned host slab, every step")}
 
 
 def dist_arm(args, wl, world, rank, local):

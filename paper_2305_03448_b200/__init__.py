@@ -26,7 +26,7 @@ __all__ = [
     "desc_scan_workspace", "SCAN_ALGO", "desc_read_probe", "desc_read_probe_sink_bytes",
     "desc_slab_transpose_peer",
     "block_reduce", "scan", "desc_transpose_host_workspace",
-    "desc_transpose_host_workspace_batched",
+    "desc_transpose_host_workspace_batched", "desc_copy2d",
     "transpose", "transpose_batched", "transpose_host",
 ]
 
@@ -93,6 +93,9 @@ def load():
     lib.desc_transpose_host.restype = ci
     lib.desc_transpose_host_workspace.argtypes = [i64, i64, ci]
     lib.desc_transpose_host_workspace.restype = ctypes.c_size_t
+    lib.desc_copy2d.argtypes = [vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_size_t,
+                                ctypes.c_size_t, vp]
+    lib.desc_copy2d.restype = ci
     lib.desc_transpose_host_workspace_batched.argtypes = [i64, i64, i64, ci]
     lib.desc_transpose_host_workspace_batched.restype = ctypes.c_size_t
     lib.desc_copy_batched.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ci, vp]
@@ -180,6 +183,11 @@ def desc_transpose_host(h_in_ptr, h_out_ptr, batch, rows, cols, ld_in, ld_out, s
 
 def desc_transpose_host_workspace(rows, cols, dtype) -> int:
     return load().desc_transpose_host_workspace(rows, cols, _dt(dtype))
+
+
+def desc_copy2d(dst, dpitch, src, spitch, width, height, stream=0):
+    """2-D copy of `height` rows of `width` bytes (host <-> device or device <-> device)."""
+    return _check(load().desc_copy2d(dst, dpitch, src, spitch, width, height, stream))
 
 
 def desc_transpose_host_workspace_batched(batch, rows, cols, dtype) -> int:

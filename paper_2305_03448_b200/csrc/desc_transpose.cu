@@ -2067,6 +2067,19 @@ size_t desc_transpose_host_workspace(int64_t rows, int64_t cols, desc_dtype dtyp
     return (size_t)(a > b ? a : b);
 }
 
+desc_status desc_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch,
+                        size_t width, size_t height, void *stream) {
+    g_last_launches = 0;
+    if (width == 0 || height == 0) return DESC_OK;
+    if (!dst || !src) return fail(DESC_ERR_NULL, "null %s pointer", dst ? "src" : "dst");
+    if (width > spitch || width > dpitch)
+        return fail(DESC_ERR_SHAPE, "width %zu exceeds a pitch (%zu, %zu)", width, spitch, dpitch);
+    cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                      static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync");
+    return DESC_OK;
+}
+
 size_t desc_transpose_host_workspace_batched(int64_t batch, int64_t rows, int64_t cols,
                                              desc_dtype dtype) {
     const size_t one = desc_transpose_host_workspace(rows, cols, dtype);

@@ -106,6 +106,17 @@ def default_chunks(Rm: int, P: int) -> int:
     return 1
 
 
+def default_host_chunks(Rm: int, es: int) -> int:
+    """Pipeline depth of the host-buffer path: the most chunks (16, 8, 4, 2) that divide Rm
+    and keep the 2-D D2H rows (the output column stripes) >= 2 KB; measured through a
+    one-rank NCCL group, 16384^2 f32: C = 2 / 4 / 8 / 16 -> 53 / 68 / 69 / 72 GB/s against 54
+    unpipelined (scripts/exp_slab_host.py, profiles/r02_exp_slab_host.txt)."""
+    for C in (16, 8, 4, 2):
+        if Rm % C == 0 and (Rm // C) * es >= 2048:
+            return C
+    return 1
+
+
 def slab_transpose(in_slab: torch.Tensor, out_slab: torch.Tensor | None = None, group=None,
                    local_transpose=None, local_copy=None, workspace=None, chunks=None,
                    all_to_all=None):
@@ -165,6 +176,105 @@ def slab_transpose(in_slab: torch.Tensor, out_slab: torch.Tensor | None = None, 
         recv_k = recv[k * N * c:(k + 1) * N * c].view(P, Rn, c)
         local_copy(recv_k, out_slab, P, Rn, c, M, k * c, Rm)   # out_r[:, s*Rm + k*c ..] = recv_k[s]
     return out_slab
+
+
+_HOST_STREAMS = {}
+
+
+def _host_streams(device):
+    """(H2D, D2H) side streams of the host-buffer pipeline, one pair per device."""
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    if key not in _HOST_STREAMS:
+        _HOST_STREAMS[key] = (torch.cuda.Stream(device), torch.cuda.Stream(device))
+    return _HOST_STREAMS[key]
+
+
+def slab_transpose_host(h_in: torch.Tensor, h_out: torch.Tensor, in_slab: torch.Tensor,
+                        out_slab: torch.Tensor, group=None, workspace=None, chunks=None,
+                        all_to_all=None, work=None):
+    """``slab_transpose`` from and to HOST memory, with the PCIe copies inside the pipeline.
+
+    h_in: (Rm, N) pinned host tensor, this rank's input rows; h_out: (Rn, M) pinned host
+    tensor for this rank's output rows; in_slab / out_slab: device staging of the same shapes
+    (workspace / all_to_all as in ``slab_transpose``).  The slab is cut into C row chunks:
+    the H2D copy of chunk k (contiguous rows) runs on its own stream and the compute stream
+    waits for it only before transposing chunk k, so later chunks' H2D overlap the earlier
+    chunks' transposes and all-to-alls; after chunk k is unpacked -- output columns
+    [s*Rm + k*c, +c) of every block s -- its P column stripes go back with 2-D D2H copies
+    (``desc_copy2d``) on a third stream, overlapping the later chunks.  The caller's current
+    stream is made to wait for the last D2H: asynchronous and stream-ordered like the rest of
+    the library.  chunks: C (default ``default_host_chunks``).  One rank without ``chunks``:
+    the banded ``desc_transpose_host`` (work: its device workspace, allocated if None)."""
+    P = dist.get_world_size(group) if dist.is_initialized() else 1
+    r = dist.get_rank(group) if dist.is_initialized() else 0
+    Rm, N = in_slab.shape
+    lay = SlabLayout(Rm * P, N, P, r)
+    Rn, M = lay.Rn, lay.M
+    if h_in.is_cuda or h_out.is_cuda:
+        raise ValueError("h_in / h_out must be host tensors")
+    if tuple(h_in.shape) != (Rm, N) or tuple(h_out.shape) != (Rn, M):
+        raise ValueError(f"h_in must be {(Rm, N)} and h_out {(Rn, M)}")
+    if not (h_in.is_contiguous() and h_out.is_contiguous() and out_slab.is_contiguous()):
+        raise ValueError("h_in, h_out and out_slab must be contiguous")
+    dev = in_slab.device
+    compute = torch.cuda.current_stream(dev)
+    if P == 1 and chunks is None:
+        if work is None:
+            work = torch.empty(desc.desc_transpose_host_workspace(Rm, N, in_slab.dtype),
+                               dtype=torch.uint8, device=dev)
+        desc.desc_transpose_host(h_in.data_ptr(), h_out.data_ptr(), 1, Rm, N, N, Rm, 0, 0,
+                                 in_slab.dtype, work.data_ptr(), work.numel(),
+                                 compute.cuda_stream)
+        return h_out
+    all_to_all = all_to_all or dist.all_to_all_single
+    es = in_slab.element_size()
+    C = default_host_chunks(Rm, es) if chunks is None else int(chunks)
+    if C < 1 or Rm % C:
+        raise ValueError(f"chunks={C} must divide the slab rows Rm={Rm}")
+    c = Rm // C
+    if workspace is None:
+        send = torch.empty(N * Rm, dtype=in_slab.dtype, device=dev)
+        recv = torch.empty(N * Rm, dtype=in_slab.dtype, device=dev)
+    else:
+        send, recv = (w.view(-1) for w in workspace)
+    h2d, d2h = _host_streams(dev)
+    h2d.wait_stream(compute)               # stream order: everything before the call
+    d2h.wait_stream(compute)
+    landed = []
+    for k in range(C):
+        with torch.cuda.stream(h2d):
+            in_slab[k * c:(k + 1) * c].copy_(h_in[k * c:(k + 1) * c], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        landed.append(ev)
+    works = []
+
+    def finish(k):                         # unpack chunk k, then its D2H on the side stream
+        works[k].wait()
+        recv_k = recv[k * N * c:(k + 1) * N * c].view(P, Rn, c)
+        _cuda_unpack(recv_k, out_slab, P, Rn, c, M, k * c, Rm)
+        ev = torch.cuda.Event()
+        ev.record(compute)
+        d2h.wait_event(ev)
+        for s_ in range(P):                # column stripe of block s_: Rn rows x c cells
+            off = (s_ * Rm + k * c) * es
+            desc.desc_copy2d(h_out.data_ptr() + off, M * es, out_slab.data_ptr() + off, M * es,
+                             c * es, Rn, d2h.cuda_stream)
+
+    # compute-stream order: pack k, then unpack k - 1 -- so the D2H of chunk k - 1 starts
+    # while chunk k + 1 is still arriving (all packs first would hold every D2H back until
+    # the last H2D had landed)
+    for k in range(C):
+        compute.wait_event(landed[k])
+        send_k = send[k * N * c:(k + 1) * N * c]
+        recv_k = recv[k * N * c:(k + 1) * N * c]
+        _cuda_transpose(in_slab[k * c:(k + 1) * c], send_k.view(N, c))
+        works.append(all_to_all(recv_k, send_k, group=group, async_op=True))
+        if k >= 1:
+            finish(k - 1)
+    finish(C - 1)
+    compute.wait_stream(d2h)
+    return h_out
 
 
 class PeerSlabTranspose:

@@ -149,6 +149,16 @@ def _nccl_path_worker(rank, world, port, M, N, es, q):
                                  all_to_all=_staged_all_to_all)
             torch.cuda.synchronize()
             ok &= out.cpu().numpy().view(A.dtype).tobytes() == exp
+        # the host-buffer pipeline (H2D chunks, exchange, 2-D D2H of the column stripes)
+        h_in = slab.cpu().pin_memory()
+        for C in (1, 2, 4):
+            h_out = torch.full((Rn, M), -1, dtype=slab.dtype).pin_memory()
+            x = torch.zeros_like(slab)
+            out = torch.zeros((Rn, M), dtype=slab.dtype, device="cuda")
+            ddist.slab_transpose_host(h_in, h_out, x, out, workspace=ws, chunks=C,
+                                      all_to_all=_staged_all_to_all)
+            torch.cuda.synchronize()
+            ok &= h_out.numpy().view(A.dtype).tobytes() == exp
         q.put((rank, bool(ok)))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
@@ -189,6 +199,16 @@ def _nccl_one_rank_worker(port, q):
                 ddist.slab_transpose(x, out, chunks=C)
             torch.cuda.synchronize()
             res.append(out.cpu().numpy().view(np.uint32).tobytes() == oracle.transpose(A).tobytes())
+            # host-buffer pipeline through the real NCCL stream ordering (and C = None at one
+            # rank: desc_transpose_host)
+            h_in = torch.from_numpy(A.view(np.int32)).pin_memory()
+            for CC in (C, None):
+                h_out = torch.full((N, M), -1, dtype=torch.int32).pin_memory()
+                for _ in range(3):
+                    ddist.slab_transpose_host(h_in, h_out, torch.empty_like(x),
+                                              torch.empty_like(out), chunks=CC)
+                torch.cuda.synchronize()
+                res.append(h_out.numpy().view(np.uint32).tobytes() == oracle.transpose(A).tobytes())
         q.put(all(res))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put(repr(e))
