@@ -1005,7 +1005,7 @@ def dist_e2e(world, rank, dev, n, steps: int = 5):
             return desc.desc_last_launch_count()
         # the host-buffer pipeline: H2D chunks, the chunked exchange, 2-D D2H stripes
         ddist.slab_transpose_host(h_in, h_out, x, out, workspace=ws, all_to_all=a2a)
-        return 2 * ddist.default_host_chunks(lay.Rm, 4)
+        return 2 * ddist.default_host_chunks(lay.Rn, 4)
     ms, launches, _ = timed_region(step, steps, 3, dev, world)
     out.copy_(h_out)                   # what reached the host, verified on the device
     parity = slab_verify(lay, out, dev, blocks=1)

@@ -173,7 +173,7 @@ desc_status desc_transpose_host(const void *h_in, void *h_out, int64_t batch,
 /* 2-D copy of `height` rows of `width` bytes between any two memory spaces (host <-> device,
  * device <-> device; direction inferred through unified addressing), asynchronous on
  * `stream`: the host-buffer slab pipeline's (paper_2305_03448_b200/dist.py
- * slab_transpose_host) D2H of output column stripes.  Plumbing, no method arithmetic.
+ * slab_transpose_host) H2D of input column stripes.  Plumbing, no method arithmetic.
  * width > spitch or width > dpitch gives DESC_ERR_SHAPE; null pointers DESC_ERR_NULL; a zero
  * width or height is a no-op. */
 desc_status desc_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch,

@@ -106,13 +106,12 @@ def default_chunks(Rm: int, P: int) -> int:
     return 1
 
 
-def default_host_chunks(Rm: int, es: int) -> int:
-    """Pipeline depth of the host-buffer path: the most chunks (16, 8, 4, 2) that divide Rm
-    and keep the 2-D D2H rows (the output column stripes) >= 2 KB; measured through a
-    one-rank NCCL group, 16384^2 f32: C = 2 / 4 / 8 / 16 -> 53 / 68 / 69 / 72 GB/s against 54
-    unpipelined (scripts/exp_slab_host.py, profiles/r02_exp_slab_host.txt)."""
+def default_host_chunks(Rn: int, es: int) -> int:
+    """Pipeline depth of the host-buffer path: the most chunks (16, 8, 4, 2) that divide the
+    block width Rn and keep each block's strided H2D rows >= 2 KB
+    (profiles/r02_exp_slab_host.txt)."""
     for C in (16, 8, 4, 2):
-        if Rm % C == 0 and (Rm // C) * es >= 2048:
+        if Rn % C == 0 and (Rn // C) * es >= 2048:
             return C
     return 1
 
@@ -196,15 +195,19 @@ def slab_transpose_host(h_in: torch.Tensor, h_out: torch.Tensor, in_slab: torch.
 
     h_in: (Rm, N) pinned host tensor, this rank's input rows; h_out: (Rn, M) pinned host
     tensor for this rank's output rows; in_slab / out_slab: device staging of the same shapes
-    (workspace / all_to_all as in ``slab_transpose``).  The slab is cut into C row chunks:
-    the H2D copy of chunk k (contiguous rows) runs on its own stream and the compute stream
-    waits for it only before transposing chunk k, so later chunks' H2D overlap the earlier
-    chunks' transposes and all-to-alls; after chunk k is unpacked -- output columns
-    [s*Rm + k*c, +c) of every block s -- its P column stripes go back with 2-D D2H copies
-    (``desc_copy2d``) on a third stream, overlapping the later chunks.  The caller's current
-    stream is made to wait for the last D2H: asynchronous and stream-ordered like the rest of
-    the library.  chunks: C (default ``default_host_chunks``).  One rank without ``chunks``:
-    the banded ``desc_transpose_host`` (work: its device workspace, allocated if None)."""
+    (workspace / all_to_all as in ``slab_transpose``).  The pipeline runs over C COLUMN chunks
+    of every block (d = Rn / C columns of block s = input columns s*Rn + k*d ..): chunk k's
+    output is rows [k*d, (k+1)*d) of this rank's output slab -- contiguous on the host -- so
+    the H2D copies are 2-D (P stripes of Rm rows x d cells, the direction PCIe handles better,
+    DESIGN §7 "band axis") and the D2H copy of each chunk is one contiguous block:
+      side stream  : H2D of chunk k (``desc_copy2d``)                    -> event
+      compute      : wait chunk k; transpose its P sub-blocks (Rm x d -> d x Rm, one batched
+                     launch) into the send buffer; asynchronous all-to-all; then unpack chunk
+                     k - 1 (d rows x Rm cells from every source, side by side)  -> event
+      third stream : D2H of the unpacked rows of chunk k - 1 (contiguous)
+    The caller's current stream waits for the last D2H: asynchronous and stream-ordered like
+    the rest of the library.  chunks: C (default ``default_host_chunks``).  One rank without
+    ``chunks``: the banded ``desc_transpose_host`` (work: its device workspace)."""
     P = dist.get_world_size(group) if dist.is_initialized() else 1
     r = dist.get_rank(group) if dist.is_initialized() else 0
     Rm, N = in_slab.shape
@@ -214,8 +217,9 @@ def slab_transpose_host(h_in: torch.Tensor, h_out: torch.Tensor, in_slab: torch.
         raise ValueError("h_in / h_out must be host tensors")
     if tuple(h_in.shape) != (Rm, N) or tuple(h_out.shape) != (Rn, M):
         raise ValueError(f"h_in must be {(Rm, N)} and h_out {(Rn, M)}")
-    if not (h_in.is_contiguous() and h_out.is_contiguous() and out_slab.is_contiguous()):
-        raise ValueError("h_in, h_out and out_slab must be contiguous")
+    if not (h_in.is_contiguous() and h_out.is_contiguous() and in_slab.is_contiguous()
+            and out_slab.is_contiguous()):
+        raise ValueError("h_in, h_out, in_slab and out_slab must be contiguous")
     dev = in_slab.device
     compute = torch.cuda.current_stream(dev)
     if P == 1 and chunks is None:
@@ -228,47 +232,54 @@ def slab_transpose_host(h_in: torch.Tensor, h_out: torch.Tensor, in_slab: torch.
         return h_out
     all_to_all = all_to_all or dist.all_to_all_single
     es = in_slab.element_size()
-    C = default_host_chunks(Rm, es) if chunks is None else int(chunks)
-    if C < 1 or Rm % C:
-        raise ValueError(f"chunks={C} must divide the slab rows Rm={Rm}")
-    c = Rm // C
+    C = default_host_chunks(Rn, es) if chunks is None else int(chunks)
+    if C < 1 or Rn % C:
+        raise ValueError(f"chunks={C} must divide the block width Rn={Rn}")
+    d = Rn // C
     if workspace is None:
         send = torch.empty(N * Rm, dtype=in_slab.dtype, device=dev)
         recv = torch.empty(N * Rm, dtype=in_slab.dtype, device=dev)
     else:
         send, recv = (w.view(-1) for w in workspace)
+        if send.numel() < N * Rm or recv.numel() < N * Rm:
+            raise ValueError("workspace tensors need N * Rm elements each")
     h2d, d2h = _host_streams(dev)
     h2d.wait_stream(compute)               # stream order: everything before the call
     d2h.wait_stream(compute)
     landed = []
-    for k in range(C):
-        with torch.cuda.stream(h2d):
-            in_slab[k * c:(k + 1) * c].copy_(h_in[k * c:(k + 1) * c], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(h2d)
+    for k in range(C):                     # H2D: P stripes of Rm rows x d cells per chunk
+        for s_ in range(P):
+            off = (s_ * Rn + k * d) * es
+            desc.desc_copy2d(in_slab.data_ptr() + off, N * es, h_in.data_ptr() + off, N * es,
+                             d * es, Rm, h2d.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(h2d)
         landed.append(ev)
     works = []
+    piece = P * d * Rm                     # elements of one chunk's send / recv buffer
 
-    def finish(k):                         # unpack chunk k, then its D2H on the side stream
+    def finish(k):                         # unpack chunk k, then its D2H on the third stream
         works[k].wait()
-        recv_k = recv[k * N * c:(k + 1) * N * c].view(P, Rn, c)
-        _cuda_unpack(recv_k, out_slab, P, Rn, c, M, k * c, Rm)
+        # from source rank q: d x Rm cells -> out rows k*d.., columns q*Rm..
+        desc.desc_copy_batched(recv.data_ptr() + k * piece * es,
+                               out_slab.data_ptr() + k * d * M * es, P, d, Rm, Rm, M, d * Rm,
+                               Rm, out_slab.dtype, compute.cuda_stream)
         ev = torch.cuda.Event()
         ev.record(compute)
         d2h.wait_event(ev)
-        for s_ in range(P):                # column stripe of block s_: Rn rows x c cells
-            off = (s_ * Rm + k * c) * es
-            desc.desc_copy2d(h_out.data_ptr() + off, M * es, out_slab.data_ptr() + off, M * es,
-                             c * es, Rn, d2h.cuda_stream)
+        with torch.cuda.stream(d2h):
+            h_out[k * d:(k + 1) * d].copy_(out_slab[k * d:(k + 1) * d], non_blocking=True)
 
-    # compute-stream order: pack k, then unpack k - 1 -- so the D2H of chunk k - 1 starts
-    # while chunk k + 1 is still arriving (all packs first would hold every D2H back until
-    # the last H2D had landed)
+    # compute-stream order: pack k, then unpack k - 1 -- the D2H of chunk k - 1 starts while
+    # chunk k + 1 is still arriving (all packs first would hold every D2H back until the last
+    # H2D had landed: no overlap, profiles/r02_exp_slab_host.txt)
     for k in range(C):
         compute.wait_event(landed[k])
-        send_k = send[k * N * c:(k + 1) * N * c]
-        recv_k = recv[k * N * c:(k + 1) * N * c]
-        _cuda_transpose(in_slab[k * c:(k + 1) * c], send_k.view(N, c))
+        send_k = send[k * piece:(k + 1) * piece]
+        recv_k = recv[k * piece:(k + 1) * piece]
+        # sub-block s (Rm x d at input column s*Rn + k*d) -> send_k[s] = its transpose (d x Rm)
+        desc.desc_transpose_batched(in_slab.data_ptr() + k * d * es, send_k.data_ptr(), P, Rm, d,
+                                    N, Rm, Rn, d * Rm, in_slab.dtype, compute.cuda_stream)
         works.append(all_to_all(recv_k, send_k, group=group, async_op=True))
         if k >= 1:
             finish(k - 1)
