@@ -30,6 +30,9 @@ Two implementations:
   land in the peers' HBM), NVLink S (P-1)/P.  A group barrier after the kernels orders the
   writes before anyone reads its slab.
 
+``slab_transpose_host`` is the NCCL path from and to pinned HOST buffers with the PCIe copies
+inside the pipeline (column chunks: strided H2D, contiguous D2H; bench.py's N > 1 e2e).
+
 The local steps are injectable (``local_transpose``/``local_copy``) only so the exchange
 logic can be tested on CPU with the gloo backend (tests/test_dist_cpu.py); the product
 default is the CUDA library, and CUDA tensors are required.
