@@ -41,67 +41,6 @@ namespace desc {
 #ifndef DESC_TILED_L2PF          // L2 prefetch of the first tile before griddepcontrol.wait
 #define DESC_TILED_L2PF 1
 #endif
-// r03 A/B knobs (scripts/build_tiled_variants.py; the defaults are the product kernel):
-#ifndef DESC_TILED_CPA           // 1: full tiles staged with cp.async (LDGSTS, 4/8-byte cells)
-#define DESC_TILED_CPA 0
-#endif
-#ifndef DESC_TILED_RASTER        // G > 0: tiles walk down tile columns inside bands of G tile rows
-#define DESC_TILED_RASTER 0
-#endif
-#ifndef DESC_TILED_LD            // input loads: 0 plain, 1 .cs (streaming), 2 .cg, 3 .lu
-#define DESC_TILED_LD 0
-#endif
-#ifndef DESC_TILED_ST            // output stores: 0 plain, 1 .cs (streaming), 2 .cg, 3 .wt
-#define DESC_TILED_ST 0
-#endif
-#ifndef DESC_TILED_MINB          // __launch_bounds__ min blocks for 256-thread CTAs
-#define DESC_TILED_MINB 5
-#endif
-
-template <typename Cell>
-__device__ __forceinline__ Cell tiled_ld(const Cell *p) {
-#if DESC_TILED_LD == 1
-    return __ldcs(p);
-#elif DESC_TILED_LD == 2
-    return __ldcg(p);
-#elif DESC_TILED_LD == 3
-    return __ldlu(p);
-#else
-    return *p;
-#endif
-}
-
-template <typename Cell>
-__device__ __forceinline__ void tiled_st(Cell *p, Cell v) {
-#if DESC_TILED_ST == 1
-    __stcs(p, v);
-#elif DESC_TILED_ST == 2
-    __stcg(p, v);
-#elif DESC_TILED_ST == 3
-    __stwt(p, v);
-#else
-    *p = v;
-#endif
-}
-
-// tile index t -> (matrix, tile row, tile col)
-__device__ __forceinline__ void tiled_coords(int64_t t, int64_t tiles_r, int64_t tiles_c,
-                                             int64_t &bt, int64_t &ti, int64_t &tj) {
-    const int64_t per = tiles_r * tiles_c;
-    bt = t / per;
-    const int64_t tm = t - bt * per;
-#if DESC_TILED_RASTER > 0
-    const int64_t band = (int64_t)DESC_TILED_RASTER * tiles_c;
-    const int64_t g = tm / band, w = tm - g * band;
-    const int64_t gr = tiles_r - g * DESC_TILED_RASTER;
-    const int64_t nr = gr < DESC_TILED_RASTER ? gr : DESC_TILED_RASTER;
-    ti = g * DESC_TILED_RASTER + w % nr;
-    tj = w / nr;
-#else
-    ti = tm / tiles_c;
-    tj = tm - ti * tiles_c;
-#endif
-}
 
 // Tile TR x TC cells, NT threads (NW = NT/32 warps).  Loads: lane tx takes columns tx + 32g
 // (g < TC/32) of rows ty + NW*k (k < TR/NW), all issued before the first shared store.
@@ -144,7 +83,7 @@ struct TiledScatter {
 #define DESC_TILED_MINB128 0
 #endif
 template <typename Cell, int TR_ = 0, int TC_ = 0, int NT_ = 256, bool SCATTER = false>
-__global__ void __launch_bounds__(NT_, NT_ >= 256 ? DESC_TILED_MINB : DESC_TILED_MINB128)
+__global__ void __launch_bounds__(NT_, NT_ >= 256 ? 5 : DESC_TILED_MINB128)
 transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int64_t rows,
                        int64_t cols, int64_t ld_in, int64_t ld_out, int64_t stride_in,
                        int64_t stride_out, int64_t tiles_r, int64_t tiles_c, int64_t ntiles,
@@ -156,17 +95,12 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
     Cell(*tile)[TC + 1] = reinterpret_cast<Cell(*)[TC + 1]>(tiled_smem);
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int ox = tx % LPR, oy = tx / LPR;                 // copy-out lane split
+    const int64_t tiles_per_mat = tiles_r * tiles_c;
     // this CTA's first tile (computed once: used by the prefetch and the first iteration)
     int64_t t = blockIdx.x;
-#if DESC_TILED_RASTER > 0
-    int64_t bt, ti, tj;
-    tiled_coords(t, tiles_r, tiles_c, bt, ti, tj);
-#else
-    const int64_t tiles_per_mat = tiles_r * tiles_c;
     int64_t bt = t / tiles_per_mat;
     int64_t ti = (t - bt * tiles_per_mat) / tiles_c;
     int64_t tj = t - bt * tiles_per_mat - ti * tiles_c;
-#endif
 #if DESC_TILED_L2PF
     // While a previous grid may still run (PDL), warm L2 with this CTA's first input tile:
     // one prefetch per 128-byte line of its rows, no data to the SM, no ordering needed --
@@ -191,13 +125,9 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
     ptx::grid_launch_dependents();
     for (; t < ntiles; t += gridDim.x) {
         if (t != (int64_t)blockIdx.x) {
-#if DESC_TILED_RASTER > 0
-            tiled_coords(t, tiles_r, tiles_c, bt, ti, tj);
-#else
             bt = t / tiles_per_mat;
             ti = (t - bt * tiles_per_mat) / tiles_c;
             tj = t - bt * tiles_per_mat - ti * tiles_c;
-#endif
         }
         const int64_t r0 = ti * TR, c0 = tj * TC;
         const Cell *src = in + bt * stride_in + r0 * ld_in + c0;
@@ -211,30 +141,14 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
         const bool full = r0 + TR <= rows && c0 + TC <= cols;
         Cell v[RK][CW];
         if (full) {
-#if DESC_TILED_CPA
-          if constexpr (sizeof(Cell) == 4 || sizeof(Cell) == 8) {
 #pragma unroll
             for (int k = 0; k < RK; ++k)
 #pragma unroll
-                for (int g = 0; g < CW; ++g)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;"
-                                 ::"r"(ptx::smem_u32(&tile[ty + NW * k][tx + 32 * g])),
-                                   "l"(src + (int64_t)(ty + NW * k) * ld_in + tx + 32 * g),
-                                   "n"((int)sizeof(Cell)) : "memory");
-            asm volatile("cp.async.wait_all;" ::: "memory");
-          } else
-#endif
-          {
-#pragma unroll
-            for (int k = 0; k < RK; ++k)
-#pragma unroll
-                for (int g = 0; g < CW; ++g)
-                    v[k][g] = tiled_ld(src + (int64_t)(ty + NW * k) * ld_in + tx + 32 * g);
+                for (int g = 0; g < CW; ++g) v[k][g] = src[(int64_t)(ty + NW * k) * ld_in + tx + 32 * g];
 #pragma unroll
             for (int k = 0; k < RK; ++k)
 #pragma unroll
                 for (int g = 0; g < CW; ++g) tile[ty + NW * k][tx + 32 * g] = v[k][g];
-          }
         } else {
             const int nr = (int)(rows - r0 < TR ? rows - r0 : TR);
             const int nc = (int)(cols - c0 < TC ? cols - c0 : TC);
@@ -261,8 +175,8 @@ transpose_tiled_kernel(const Cell *__restrict__ in, Cell *__restrict__ out, int6
 #pragma unroll
                 for (int h = 0; h < OH; ++h) {
                     const int oc = RPI * (ty + NW * m) + oy, orr = ox + LPR * h;
-                    tiled_st(dst + (int64_t)oc * ld_out + orr,
-                             DESC_MUTANT(MUT_TILED_TILE_ONLY) ? tile[oc][orr] : tile[orr][oc]);
+                    dst[(int64_t)oc * ld_out + orr] =
+                        DESC_MUTANT(MUT_TILED_TILE_ONLY) ? tile[oc][orr] : tile[orr][oc];
                 }
         } else {
             const int nr = (int)(rows - r0 < TR ? rows - r0 : TR);

@@ -86,9 +86,6 @@ struct CellIO {
 #ifndef DESC_VIEW_UNR         // rows' loads in flight per thread in the short-row path (A/B)
 #define DESC_VIEW_UNR 4
 #endif
-#ifndef DESC_VIEW_PF1         // A/B: compile the first-item prefetch into MODE 1 too
-#define DESC_VIEW_PF1 0
-#endif
 // MODE 1 keeps 4 CTAs/SM (<= 64 registers) under its persistent grid: residency is what
 // keeps its loads in flight (74 registers = 3 CTAs/SM cost the tile view 0.95 -> 0.82).
 template <typename Cell, int MODE>
@@ -98,7 +95,7 @@ view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const Vie
     using IO = CellIO<Cell, MODE>;
     using T = typename IO::T;
     constexpr int CB = IO::CB;
-    if constexpr (MODE == 2 || (MODE == 1 && DESC_VIEW_PF1)) {
+    if constexpr (MODE == 2) {
         // mirrored rows (reverse views), launched one work item per CTA: L2 prefetch of the
         // item's input rows, one per 128-byte line, before the dependency wait (as TILED,
         // tiled_transpose.cuh: L2 is the point of coherence, a prefetch returns nothing to
@@ -113,9 +110,8 @@ view_tiles_kernel(const char *__restrict__ in, char *__restrict__ out, const Vie
             const int64_t V = 16 / es, lpr = (nu * 16 + 127) / 128;     // lines per row
             for (int64_t i = threadIdx.x; i < nr * lpr; i += blockDim.x) {
                 const int64_t rr = r0 + i / lpr, l = i % lpr;
-                // first input element of the row segment (MODE 2 walks it backwards)
-                const int64_t e0 = MODE == 1 ? obase + rr * v.s2 + u0 * V
-                                             : obase + rr * v.s2 - (u0 + nu) * V + 1;
+                // first input element of the row segment (walked backwards)
+                const int64_t e0 = obase + rr * v.s2 - (u0 + nu) * V + 1;
                 ptx::prefetch_l2(in + e0 * es + l * 128);
             }
         }

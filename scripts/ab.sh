@@ -5,6 +5,8 @@
 # each experiment prints the lines its profiles/r02_*.txt record holds.
 
 tiled_variants() {
+  # (the TILED knobs these variants used were removed after the recorded run; see
+  #  scripts/build_tiled_variants.py)
   # r03 TILED A/B: product vs compile-time variants (scripts/build_tiled_variants.py), interleaved
   #   bash scripts/ab.sh tiled_variants "<variants>" "<shapes>" <rounds>
   V=${1:-"cpa5 cpa8 r4 r8 r16 r32 ldcs ldlu stcs stcg ldcs_stcs minb6"}

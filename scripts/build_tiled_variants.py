@@ -12,25 +12,16 @@ VARIANTS = {
     "s1": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=64"],
     "s2": ["DESC_TILED_TR8=64", "DESC_TILED_TC8=32"],
     "s3": ["DESC_TILED_TR8=32", "DESC_TILED_TC8=32"],
-    # r03: cp.async staging, banded raster orders, cache hints, occupancy
-    "cpa5": ["DESC_TILED_CPA=1"],
-    "cpa8": ["DESC_TILED_CPA=1", "DESC_TILED_MINB=8"],
-    "r4": ["DESC_TILED_RASTER=4"],
-    "r8": ["DESC_TILED_RASTER=8"],
-    "r16": ["DESC_TILED_RASTER=16"],
-    "r32": ["DESC_TILED_RASTER=32"],
-    "ldcs": ["DESC_TILED_LD=1"],
-    "ldlu": ["DESC_TILED_LD=3"],
-    "stcs": ["DESC_TILED_ST=1"],
-    "stcg": ["DESC_TILED_ST=2"],
-    "ldcs_stcs": ["DESC_TILED_LD=1", "DESC_TILED_ST=1"],
-    "minb6": ["DESC_TILED_MINB=6"],
+    # (r02 session 2: the TILED knobs for cp.async staging, banded raster orders, load / store
+    # cache hints and 6 CTAs/SM were measured -- profiles/r02_tiled_variants_cpasync_raster_hints.txt
+    # -- none won, and they were removed from tiled_transpose.cuh again)
     # r02 (session 2): the 16-byte vector tile kernel without cp.async (LDG.128 -> STS.128)
     "vt_nocpa": ["DESC_VT_CPA=0"],
     # TMA ring slot release after ld.shared without the proxy fence (ptx.cuh)
     "rel0": ["DESC_REL_MODE=0"],
     # view copies: first-item prefetch compiled into the plain 16-byte mode
-    "viewpf1": ["DESC_VIEW_PF1=1"],
+    # (viewpf1, DESC_VIEW_PF1=1: the first-item prefetch in the plain view mode -- lost,
+    #  profiles/r02_view_tiles_pf1.txt -- the knob was removed again)
     "viewunr8": ["DESC_VIEW_UNR=8"],
     "vtminb10": ["DESC_VT_MINB=10"],
     "vtminb12": ["DESC_VT_MINB=12"],
