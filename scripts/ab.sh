@@ -111,6 +111,7 @@ view_grid() {
 }
 
 view_pf1() {
+  # (the viewpf1 build's knob was removed after the recorded run: scripts/build_tiled_variants.py)
   # r02 (session 2): the plain 16-byte view mode (group_by_tile) with the first-item L2 prefetch
   # compiled in (viewpf1 build), persistent vs one item per CTA
   for r in 1 2; do
