@@ -19,6 +19,7 @@ VARIANTS = {
     "lc_i32_nr8": ["DESC_SCAN_LC_I32=1", "DESC_SCAN_LC_I32_NR=8"],
     "lc_f64": ["DESC_SCAN_LC_F64=1"],
     "relnofence": ["DESC_SCAN_REL_FENCE=0"],
+    "lc_u8": ["DESC_SCAN_LC_U8=1"],
     # look-back knobs on the lane-contiguous kernels
     "lbw2": ["DESC_SCAN_LB_WINDOW=2"],
     "sleep64": ["DESC_SCAN_SLEEP_CAP=64"],
