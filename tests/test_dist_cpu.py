@@ -74,6 +74,37 @@ def test_default_chunks_and_bad_chunks():
         ddist.slab_transpose(x, torch.zeros((6, 6), dtype=torch.int32))
 
 
+def test_fake_ranks_column_chunked_host_pipeline():
+    """The host-buffer pipeline's exchange (dist.slab_transpose_host) restated on the CPU with
+    fake ranks: chunk k = columns [s*Rn + k*d, +d) of every block s; each block's sub-block is
+    transposed into the send buffer, exchanged, and unpacked as output rows [k*d, +d) of the
+    receiver, columns q*Rm.. from source q.  Every chunk count must rebuild every rank's
+    output slab exactly (oracle.dist_expected_slab)."""
+    P, M, N = 4, 64, 96
+    A = synth.random_bits((M, N), 4, 77)
+    Rm, Rn = M // P, N // P
+    for C in (1, 2, 3, 6):
+        d = Rn // C
+        outs = [np.zeros((Rn, M), dtype=A.dtype) for _ in range(P)]
+        for k in range(C):
+            # rank q's send buffer: P pieces (d x Rm), piece s = its block (q, s) sub-block^T
+            sends = [[oracle.transpose(A[q * Rm:(q + 1) * Rm, s * Rn + k * d:s * Rn + (k + 1) * d])
+                      for s in range(P)] for q in range(P)]
+            for s in range(P):             # receiver s gets piece s from every source q
+                for q in range(P):
+                    outs[s][k * d:(k + 1) * d, q * Rm:(q + 1) * Rm] = sends[q][s]
+        for r in range(P):
+            assert outs[r].tobytes() == oracle.dist_expected_slab(A, r, P).tobytes(), (C, r)
+
+
+def test_default_host_chunks():
+    """Most chunks (16, 8, 4, 2) dividing the block width with >= 2 KB strided H2D rows."""
+    assert ddist.default_host_chunks(16384, 4) == 16     # 1024 cells = 4 KB rows
+    assert ddist.default_host_chunks(2048, 4) == 4       # 512 cells = 2 KB
+    assert ddist.default_host_chunks(1000, 4) == 1       # no divisor keeps 2 KB rows
+    assert ddist.default_host_chunks(8192, 8) == 16
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
