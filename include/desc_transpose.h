@@ -28,8 +28,10 @@
  *   rule), in one of two layouts: stacked, stride_out >= (cols-1)*ld_out
  *   + rows; or side by side within each output row, stride_out >= rows and
  *   (batch-1)*stride_out + rows <= ld_out.  Otherwise DESC_ERR_SHAPE.  Input matrices may overlap (read-only).  Strides must be >= 0.
- *   The caller owns both buffers; the library allocates no device memory and
- *   keeps only a host-side, thread-safe cache of TMA descriptors.
+ *   The caller owns both buffers; the library allocates no device memory for data
+ *   (the one exception: a 16-byte tile counter per (device, stream) for the TMA-store
+ *   kernel's dynamic scheduler, created on first use and kept for the process) and
+ *   keeps a host-side, thread-safe cache of TMA descriptors.
  *
  * Memory space.
  *   Both pointers must be device (or managed) memory of the CURRENT device, or of a
