@@ -664,8 +664,11 @@ desc_status launch_tiled(const Args &a, const desc::TiledScatter *scatter = null
     if (scatter) sc = *scatter;
     const int64_t tiles_r = (a.rows + C::TR - 1) / C::TR, tiles_c = (a.cols + C::TC - 1) / C::TC;
     const int64_t ntiles = tiles_r * tiles_c * a.batch;
-    const int64_t max_grid = (int64_t)1 << 30;           // one tile per CTA up to 2^30 tiles
-    const int grid = (int)(ntiles < max_grid ? ntiles : max_grid);
+    // one tile per CTA up to 2^30 tiles (DESC_TILED_TPC=<k>: k tiles per CTA, A/B)
+    static const int tpc = dev_knob("DESC_TILED_TPC", 1);
+    const int64_t want = tpc > 1 ? (ntiles + tpc - 1) / tpc : ntiles;
+    const int64_t max_grid = (int64_t)1 << 30;
+    const int grid = (int)(want < max_grid ? want : max_grid);
     if (C::SMEM > 48 * 1024) {
         static std::mutex mu;                              // per device, once
         static bool opted[64] = {};

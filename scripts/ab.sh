@@ -1,6 +1,6 @@
 #!/bin/bash
 # Named A/B experiments of round 2 (each was a one-off driver; folded here).
-#   bash scripts/ab.sh <name> [args...]      names: tiled_128rows vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
+#   bash scripts/ab.sh <name> [args...]      names: tiled_tpc tiled_128rows vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048
 # Compile-time variants come from scripts/build_{tiled,scan}_variants.py (DESC_LIB=...);
 # each experiment prints the lines its profiles/r02_*.txt record holds.
 
@@ -195,5 +195,17 @@ tiled_128rows() {
   done; done
 }
 
+tiled_tpc() {
+  # r02 (session 2): TILED with k tiles per CTA (DESC_TILED_TPC) and the second tile prefetched
+  # before the dependency wait too (tiledpf2 build; its knob was removed after the run)
+  line() { python bench.py --workload $1 --steps 20 --warmup 5 --no-oracle --no-e2e --no-context 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$2', '$1', d['value'], d['roofline']['frac'])"; }
+  for r in 1 2; do for w in 8192f32 2048f64 batched; do
+    line $w "product tpc1"
+    DESC_TILED_TPC=2 line $w "product tpc2"
+    DESC_LIB=build_variants/lib_tiled_tiledpf2.so DESC_TILED_TPC=2 line $w "pf2 tpc2"
+    DESC_LIB=build_variants/lib_tiled_tiledpf2.so DESC_TILED_TPC=4 line $w "pf2 tpc4"
+  done; done
+}
+
 name=$1; shift
-case " tiled_128rows vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac
+case " tiled_tpc tiled_128rows vtiled_minb view_unroll e2e_batch tiled_variants vtiled vtiled_narrow scan_variants release e2e_axis e2e_bands copy view_grid view_pf1 view_old regress f64_2048 " in *" $name "*) "$name" "$@";; *) echo "unknown experiment: $name"; exit 2;; esac

@@ -23,6 +23,8 @@ VARIANTS = {
     # (viewpf1, DESC_VIEW_PF1=1: the first-item prefetch in the plain view mode -- lost,
     #  profiles/r02_view_tiles_pf1.txt -- the knob was removed again)
     "viewunr8": ["DESC_VIEW_UNR=8"],
+    # (tiledpf2, DESC_TILED_PF2=1: second-tile prefetch -- lost, removed again;
+    #  profiles/r02_tiled_tiles_per_cta.txt)
     "vtminb10": ["DESC_VT_MINB=10"],
     "vtminb12": ["DESC_VT_MINB=12"],
     "viewunr2": ["DESC_VIEW_UNR=2"],
